@@ -1,0 +1,58 @@
+# Product build: paper_2403_06504_b200/lib/liboffsim.so.0 (+ liboffsim.so link)
+#   - offsim core (C++20, g++): the API-compatible restatement of the
+#     reference's planner / schedule / DES / trace checks / C ABI
+#   - B200 executor (CUDA, nvcc, sm_100a only): fused Adam kernels, chunk
+#     pipeline, activation-swap copy engine, fy_* C ABI
+# `make` builds the library, the parity dump driver and the oracle .so.
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+PKG      := paper_2403_06504_b200
+LIBDIR   := $(PKG)/lib
+OBJDIR   := build/obj
+JSONDIR  ?= $(shell python3 -c "import os,sysconfig;print(os.path.join(sysconfig.get_paths()['purelib'],'include','cudnn_frontend','thirdparty','nlohmann'))")
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(JSONDIR)
+NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -Xptxas -v
+
+CORE_SRC := $(wildcard $(PKG)/csrc/core/*.cpp)
+CUDA_SRC := $(wildcard $(PKG)/csrc/cuda/*.cu)
+CORE_OBJ := $(patsubst $(PKG)/csrc/core/%.cpp,$(OBJDIR)/core/%.o,$(CORE_SRC))
+CUDA_OBJ := $(patsubst $(PKG)/csrc/cuda/%.cu,$(OBJDIR)/cuda/%.o,$(CUDA_SRC))
+HDRS     := $(wildcard include/offsim/*.hpp include/offsim/*.h include/fuyou/*.h) \
+            $(wildcard $(PKG)/csrc/core/*.hpp $(PKG)/csrc/cuda/*.cuh)
+
+all: $(LIBDIR)/liboffsim.so $(if $(CORE_SRC),build/offsim_dump) oracle
+
+$(OBJDIR)/core/%.o: $(PKG)/csrc/core/%.cpp $(HDRS)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(OBJDIR)/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/cuda/$*.ptxas.log || (cat $(OBJDIR)/cuda/$*.ptxas.log; false)
+
+build/liboffsim_core.a: $(CORE_OBJ)
+	@mkdir -p build
+	rm -f $@ && ar rcs $@ $^
+
+$(LIBDIR)/liboffsim.so.0: $(CORE_OBJ) $(CUDA_OBJ)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -Xlinker -soname=liboffsim.so.0 -o $@ $^ -lpthread
+
+$(LIBDIR)/liboffsim.so: $(LIBDIR)/liboffsim.so.0
+	ln -sf liboffsim.so.0 $@
+
+# Parity driver compiled against this repo's headers + core.
+build/offsim_dump: tests/parity/offsim_dump.cpp build/liboffsim_core.a
+	$(CXX) $(CXXFLAGS) $< build/liboffsim_core.a -pthread -o $@
+
+oracle:
+	$(MAKE) -C oracle all
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf build $(LIBDIR)
+
+.PHONY: all oracle ref clean

@@ -1,0 +1,194 @@
+/* fy_adam.h — C ABI of the B200 out-of-core Adam step (kernels + chunk
+ * pipeline). Plain pointers and sizes only; no CUDA, torch or C++ types.
+ * `stream` arguments are cudaStream_t values passed as void* (NULL = the
+ * legacy default stream).
+ *
+ * Conventions follow the reference C ABI (proj/include/offsim/offsim_c.h:
+ * 16-28, proj/src/capi.cpp:19-51): integer status codes with the same
+ * numbering, a thread-local last-error string that is never NULL, no
+ * exception crossing the boundary, NULL arguments -> FY_ERR_CONFIG. The
+ * caller owns every buffer; nothing here allocates device memory except the
+ * pipeline object (its staging slots), which fy_pipeline_destroy releases.
+ *
+ * Reference interfaces replaced (the reference prices these as DAG tasks;
+ * this library executes them):
+ *   fy_adamw_chunk       <- `opt update gK`, TaskKind::optimizer_update on
+ *                           ResourceId::cpu_compute, work = 12h^2 params
+ *                           (proj/src/task_graph.cpp:488-495; priced at
+ *                           proj/src/simulator.cpp:21,37-41)
+ *   fy_pipeline_step     <- the optimizer group block `opt state_s2c gK ->
+ *                           opt update gK -> opt state_c2s gK / opt
+ *                           param_c2s gK` with the depth-2 read gate
+ *                           (proj/src/task_graph.cpp:453-503)
+ *   fy_swap_*            <- activation swap transfers `fwd act_g2c/act_c2s`,
+ *                           `fwd ckpt_g2c/ckpt_c2s`, `bwd ckpt_s2c/ckpt_c2g`,
+ *                           `bwd act_s2c/act_c2g`
+ *                           (proj/src/task_graph.cpp:296-321,357-397)
+ */
+#ifndef FUYOU_FY_ADAM_H
+#define FUYOU_FY_ADAM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fy_status {
+    FY_OK = 0,
+    FY_ERR_CONFIG = 2,     /* bad argument / unsupported combination   */
+    FY_ERR_INFEASIBLE = 3, /* does not fit (device or host memory)     */
+    FY_ERR_INVARIANT = 4,  /* executed trace violates its graph        */
+    FY_ERR_INTERNAL = 5,
+    FY_ERR_DEVICE = 6      /* CUDA / NCCL / IO error (message in last error) */
+} fy_status;
+
+typedef enum fy_dtype { FY_BF16 = 0, FY_FP16 = 1, FY_FP32 = 2 } fy_dtype;
+
+const char* fy_version(void);
+const char* fy_last_error(void);
+
+/* Adam hyper-parameters of one step. Semantics: DeepSpeed 0.9.3
+ * DeepSpeedCPUAdam (the optimizer the paper runs):
+ * bias_correction1 = 1 - beta1^step, bias_correction2 = 1/sqrt(1-beta2^step)
+ * (beta^step evaluated in double, stored float), eps added after the
+ * bias-corrected sqrt(v), decoupled decay when adamw_mode != 0. The gradient
+ * is first multiplied by grad_scale (1/loss_scale, times a clip coefficient
+ * if the caller clips). */
+typedef struct fy_adam_hparams {
+    float lr;
+    float beta1;
+    float beta2;
+    float eps;
+    float weight_decay;
+    uint64_t step; /* 1-based step count after this update */
+    int adamw_mode;
+    int bias_correction;
+    float grad_scale;
+} fy_adam_hparams;
+
+/* One chunk (one transformer block = 12h^2 params, or a shard slice of it).
+ * master / exp_avg / exp_avg_sq: fp32 [n] device pointers, updated in place.
+ * grad: [n] of grad_dtype (bf16/fp16/fp32), device.
+ * param_out: [n] of param_dtype (bf16/fp16) or NULL; may alias grad (the
+ * reference's "gradient buffer becomes the fp16 params",
+ * task_graph.cpp:493-495).
+ * grad_sq_sum: optional device double; receives sum((grad*grad_scale)^2)
+ * (added to the existing value when accumulate_sq != 0). Requires workspace.
+ * workspace: device floats, >= fy_adamw_workspace_floats() (may be NULL when
+ * grad_sq_sum is NULL).
+ * nonfinite_flag: optional device int, set to 1 if any scaled gradient is
+ * inf/nan (never cleared by the kernel). */
+typedef struct fy_adamw_args {
+    float* master;
+    float* exp_avg;
+    float* exp_avg_sq;
+    const void* grad;
+    int grad_dtype;
+    void* param_out;
+    int param_dtype;
+    uint64_t n;
+    fy_adam_hparams hp;
+    double* grad_sq_sum;
+    int accumulate_sq;
+    float* workspace;
+    int* nonfinite_flag;
+} fy_adamw_args;
+
+uint32_t fy_adamw_workspace_floats(void);
+
+/* Fused unscale + grad-norm partial + AdamW + downcast, one launch (two when
+ * grad_sq_sum is requested: the second is a one-block ordered reduction). */
+fy_status fy_adamw_chunk(const fy_adamw_args* args, void* stream);
+
+/* Gradient statistics only (2 B/param read): sum of squares and non-finite
+ * flag, for callers that must clip or skip before any update is applied. */
+fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad_scale,
+                        double* grad_sq_sum, int accumulate_sq, float* workspace,
+                        int* nonfinite_flag, void* stream);
+
+/* Number of SMs and the launch geometry the kernels use on `device`
+ * (diagnostics / roofline bookkeeping). */
+fy_status fy_device_info(int device, int* sm_count, int* ctas_per_sm, int* threads_per_cta);
+
+/* ------------------------------------------------------------------ */
+/* Multi-GPU sharding of a chunk: chunk of n elements split
+ * into `world` contiguous slices, each a multiple of `align` elements except
+ * the last; returns [offset, count) of `rank`. Pure host arithmetic. */
+fy_status fy_shard_range(uint64_t n, uint32_t world, uint32_t rank, uint32_t align,
+                         uint64_t* offset, uint64_t* count);
+
+/* ------------------------------------------------------------------ */
+/* Chunk pipeline: streamed (out-of-core) optimizer step.
+ *
+ * The host holds each chunk's states as one contiguous pinned region
+ * [master | exp_avg | exp_avg_sq] (12n bytes) and optionally its gradients
+ * and output params. Per chunk the pipeline issues:
+ *   H2D states (copy stream)  -> fy_adamw_chunk (compute stream)
+ *   -> D2H states (+ params)  (copy stream)
+ * with `slots` device staging buffers, and the reference's depth-2 read gate
+ * (the read of chunk i waits for the update of chunk i-2,
+ * task_graph.cpp:463-471). Gradients may live on the device (produced by
+ * backward; optionally gated by a caller event) or on the host (H2D'd with
+ * the states). */
+
+typedef struct fy_pipeline fy_pipeline;
+
+typedef struct fy_pipeline_config {
+    int device;
+    uint64_t max_chunk_elems;   /* largest chunk; sizes the staging slots */
+    uint32_t slots;             /* device staging slots (>= 2; default 3) */
+    int grad_dtype;
+    int param_dtype;
+    int grads_on_host;          /* 1: grads come from pinned host memory  */
+    int params_to_host;         /* 1: D2H the downcast params to host     */
+    int keep_params_on_device;  /* 1: also write params to chunk.d_param  */
+    int states_on_device;       /* 1: chunk.h_states is a DEVICE pointer to
+                                   [master|m|v]; no state copies (the
+                                   device-resident tier; grads/params may
+                                   still cross the host link) */
+} fy_pipeline_config;
+
+typedef struct fy_chunk {
+    uint64_t n;
+    void* h_states;       /* [master|m|v], 12n bytes: pinned host, or device
+                             when states_on_device (required)              */
+    const void* grad;     /* device ptr (grads_on_host=0) or pinned host ptr */
+    void* h_param;        /* pinned host [n] params (params_to_host=1)      */
+    void* d_param;        /* device [n] params (keep_params_on_device=1)    */
+    void* grad_ready;     /* optional cudaEvent_t the update must wait on   */
+} fy_chunk;
+
+/* Per-chunk timings of the last step, in ns relative to the step start
+ * (CUDA events): h2d [start,end), update [start,end), d2h [start,end). */
+typedef struct fy_chunk_timing {
+    uint64_t h2d_start_ns, h2d_end_ns;
+    uint64_t upd_start_ns, upd_end_ns;
+    uint64_t d2h_start_ns, d2h_end_ns;
+} fy_chunk_timing;
+
+fy_status fy_pipeline_create(const fy_pipeline_config* cfg, fy_pipeline** out);
+void fy_pipeline_destroy(fy_pipeline* p);
+
+/* Runs one optimizer step over chunks[0..count) in the given order and
+ * returns when the step has been ENQUEUED; fy_pipeline_wait blocks until it
+ * completes. grad_sq_sum (optional, host double*) receives the step's sum of
+ * squared scaled gradients after fy_pipeline_wait. */
+fy_status fy_pipeline_step(fy_pipeline* p, const fy_chunk* chunks, uint32_t count,
+                           const fy_adam_hparams* hp, int want_grad_norm);
+fy_status fy_pipeline_wait(fy_pipeline* p, double* grad_sq_sum, int* nonfinite);
+
+/* Timings of the last completed step (count entries). */
+fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32_t count,
+                              uint64_t* step_ns);
+
+/* Pinned host allocation helpers (cudaHostAlloc, portable). */
+fy_status fy_host_alloc(uint64_t bytes, void** out);
+fy_status fy_host_free(void* p);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* FUYOU_FY_ADAM_H */

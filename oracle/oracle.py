@@ -1,0 +1,98 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes wrapper of oracle/_build/liboracle_adamw.so.
+
+Callers allowed: tests/, __graft_entry__.smoke(), bench.py (cpu_baseline and
+--impl reference). The product never imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+_SO = Path(__file__).resolve().parent / "_build" / "liboracle_adamw.so"
+BF16, FP16, FP32 = 0, 1, 2
+
+
+class Scalars(C.Structure):
+    _fields_ = [(k, C.c_float) for k in (
+        "beta1", "beta2", "one_minus_beta1", "one_minus_beta2", "bias_correction1",
+        "bias_correction2", "step_size", "w_decay", "eps", "weight_decay")] + [("adamw_mode", C.c_int)]
+
+
+def _load():
+    if not _SO.exists():
+        raise ImportError(f"{_SO} missing; run `make -C oracle`")
+    lib = C.CDLL(str(_SO))
+    lib.oracle_adamw_scalars.argtypes = [C.c_float] * 5 + [C.c_uint64, C.c_int, C.c_int,
+                                                           C.POINTER(Scalars)]
+    lib.oracle_adamw_scalars.restype = None
+    vp = C.c_void_p
+    lib.oracle_adamw_step.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, C.c_uint64,
+                                      C.POINTER(Scalars), C.c_float, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int)]
+    lib.oracle_adamw_step.restype = None
+    lib.oracle_adamw_step_omp.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, C.c_uint64,
+                                          C.POINTER(Scalars), C.c_float, C.c_int]
+    lib.oracle_adamw_step_omp.restype = None
+    lib.oracle_max_threads.restype = C.c_int
+    lib.oracle_first_touch.argtypes = [vp, C.c_uint64, C.c_float, C.c_int]
+    lib.oracle_float_to_bf16.argtypes = [C.c_float]
+    lib.oracle_float_to_bf16.restype = C.c_uint16
+    lib.oracle_float_to_fp16.argtypes = [C.c_float]
+    lib.oracle_float_to_fp16.restype = C.c_uint16
+    lib.oracle_bf16_to_float.argtypes = [C.c_uint16]
+    lib.oracle_bf16_to_float.restype = C.c_float
+    lib.oracle_fp16_to_float.argtypes = [C.c_uint16]
+    lib.oracle_fp16_to_float.restype = C.c_float
+    return lib
+
+
+LIB = _load()
+
+
+def scalars(lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, step=10,
+            adamw_mode=True, bias_correction=True) -> Scalars:
+    s = Scalars()
+    LIB.oracle_adamw_scalars(lr, beta1, beta2, eps, weight_decay, step, int(adamw_mode),
+                             int(bias_correction), C.byref(s))
+    return s
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def adamw_step(master: np.ndarray, m: np.ndarray, v: np.ndarray, grad: np.ndarray,
+               grad_dtype: int, s: Scalars, grad_scale: float = 1.0, param_out=None,
+               param_dtype: int = BF16):
+    """In-place scalar oracle step on numpy arrays; grads/params as uint16 bit
+    patterns for bf16/fp16 (float32 for FP32). Returns (grad_sq_sum, nonfinite)."""
+    for a in (master, m, v):
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    sq = C.c_double()
+    bad = C.c_int(0)
+    LIB.oracle_adamw_step(_p(master), _p(m), _p(v), _p(grad), grad_dtype, _p(param_out),
+                          param_dtype, master.size, C.byref(s), grad_scale, C.byref(sq),
+                          C.byref(bad))
+    return sq.value, bad.value
+
+
+def adamw_step_omp(master, m, v, grad, grad_dtype, s, grad_scale=1.0, param_out=None,
+                   param_dtype=BF16, threads=0):
+    LIB.oracle_adamw_step_omp(_p(master), _p(m), _p(v), _p(grad), grad_dtype, _p(param_out),
+                              param_dtype, master.size, C.byref(s), grad_scale, threads)
+
+
+def max_threads() -> int:
+    return int(LIB.oracle_max_threads())
+
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    f = np.vectorize(LIB.oracle_float_to_bf16, otypes=[np.uint16])
+    return f(x.astype(np.float32))
+
+
+def f32_to_fp16_bits(x: np.ndarray) -> np.ndarray:
+    f = np.vectorize(LIB.oracle_float_to_fp16, otypes=[np.uint16])
+    return f(x.astype(np.float32))

@@ -1,0 +1,112 @@
+"""ctypes binding of the product library ``lib/liboffsim.so.0``.
+
+The library is the drop-in boundary: the reference's C ABI
+(``include/offsim/offsim_c.h``) plus the B200 executor ABI
+(``include/fuyou/fy_adam.h``). This module only declares signatures; it
+never falls back to anything when the library is missing — importing the
+package on a machine without the built library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_DIR = Path(__file__).resolve().parent / "lib"
+LIB_PATH = LIB_DIR / "liboffsim.so.0"
+
+# fy_status / offsim_status share the numbering of proj/include/offsim/offsim_c.h:16-22
+FY_OK, FY_ERR_CONFIG, FY_ERR_INFEASIBLE, FY_ERR_INVARIANT, FY_ERR_INTERNAL, FY_ERR_DEVICE = (
+    0, 2, 3, 4, 5, 6)
+FY_BF16, FY_FP16, FY_FP32 = 0, 1, 2
+
+
+class FyError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"status {status}: {message}")
+        self.status = status
+
+
+class AdamHparams(C.Structure):
+    _fields_ = [
+        ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+        ("weight_decay", C.c_float), ("step", C.c_uint64), ("adamw_mode", C.c_int),
+        ("bias_correction", C.c_int), ("grad_scale", C.c_float),
+    ]
+
+
+class AdamwArgs(C.Structure):
+    _fields_ = [
+        ("master", C.c_void_p), ("exp_avg", C.c_void_p), ("exp_avg_sq", C.c_void_p),
+        ("grad", C.c_void_p), ("grad_dtype", C.c_int), ("param_out", C.c_void_p),
+        ("param_dtype", C.c_int), ("n", C.c_uint64), ("hp", AdamHparams),
+        ("grad_sq_sum", C.c_void_p), ("accumulate_sq", C.c_int), ("workspace", C.c_void_p),
+        ("nonfinite_flag", C.c_void_p),
+    ]
+
+
+class PipelineConfig(C.Structure):
+    _fields_ = [
+        ("device", C.c_int), ("max_chunk_elems", C.c_uint64), ("slots", C.c_uint32),
+        ("grad_dtype", C.c_int), ("param_dtype", C.c_int), ("grads_on_host", C.c_int),
+        ("params_to_host", C.c_int), ("keep_params_on_device", C.c_int),
+        ("states_on_device", C.c_int),
+    ]
+
+
+class Chunk(C.Structure):
+    _fields_ = [
+        ("n", C.c_uint64), ("h_states", C.c_void_p), ("grad", C.c_void_p),
+        ("h_param", C.c_void_p), ("d_param", C.c_void_p), ("grad_ready", C.c_void_p),
+    ]
+
+
+class ChunkTiming(C.Structure):
+    _fields_ = [
+        ("h2d_start_ns", C.c_uint64), ("h2d_end_ns", C.c_uint64),
+        ("upd_start_ns", C.c_uint64), ("upd_end_ns", C.c_uint64),
+        ("d2h_start_ns", C.c_uint64), ("d2h_end_ns", C.c_uint64),
+    ]
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (or `make`). There is no fallback implementation.")
+    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
+    st = C.c_int
+    sig = {
+        "fy_version": (C.c_char_p, []),
+        "fy_last_error": (C.c_char_p, []),
+        "fy_adamw_workspace_floats": (C.c_uint32, []),
+        "fy_adamw_chunk": (st, [C.POINTER(AdamwArgs), C.c_void_p]),
+        "fy_grad_stats": (st, [C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_void_p, C.c_int,
+                               C.c_void_p, C.c_void_p, C.c_void_p]),
+        "fy_device_info": (st, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                C.POINTER(C.c_int)]),
+        "fy_shard_range": (st, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "fy_pipeline_create": (st, [C.POINTER(PipelineConfig), C.POINTER(C.c_void_p)]),
+        "fy_pipeline_destroy": (None, [C.c_void_p]),
+        "fy_pipeline_step": (st, [C.c_void_p, C.POINTER(Chunk), C.c_uint32,
+                                  C.POINTER(AdamHparams), C.c_int]),
+        "fy_pipeline_wait": (st, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
+        "fy_pipeline_timings": (st, [C.c_void_p, C.POINTER(ChunkTiming), C.c_uint32,
+                                     C.POINTER(C.c_uint64)]),
+        "fy_host_alloc": (st, [C.c_uint64, C.POINTER(C.c_void_p)]),
+        "fy_host_free": (st, [C.c_void_p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = _load()
+
+
+def check(status: int) -> None:
+    if status != FY_OK:
+        raise FyError(status, LIB.fy_last_error().decode())

@@ -1,0 +1,60 @@
+// Internal interface of the fused Adam kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace fy {
+
+// Per-launch scalars, precomputed on the host exactly as DeepSpeed 0.9.3
+// cpu_adam.h update_state() does (see adamw_kernels.cu).
+struct AdamScalars {
+    float beta1, beta2;
+    float one_minus_beta1, one_minus_beta2;
+    float bias_correction2; // 1 / sqrt(1 - beta2^t)
+    float step_size;        // -lr / (1 - beta1^t)
+    float w_decay;          // -lr*wd (adamw) or wd (L2 mode)
+    float eps;
+    float grad_scale;
+    int adamw_mode;
+    int has_weight_decay;
+};
+
+AdamScalars make_scalars(float lr, float beta1, float beta2, float eps, float weight_decay,
+                         std::uint64_t step, int adamw_mode, int bias_correction,
+                         float grad_scale);
+
+struct AdamLaunch {
+    float* master;
+    float* m;
+    float* v;
+    const void* grad;
+    int grad_dtype;   // 0 bf16, 1 fp16, 2 fp32
+    void* param;      // may be null or alias grad
+    int param_dtype;  // 0 bf16, 1 fp16
+    std::uint64_t n;
+    AdamScalars s;
+    double* grad_sq_sum; // optional
+    int accumulate_sq;
+    float* workspace;    // >= kWorkspaceFloats when grad_sq_sum
+    int* nonfinite;      // optional
+};
+
+constexpr int kThreads = 256;
+constexpr std::uint32_t kWorkspaceFloats = 148u * 32u;
+
+// Enqueue the fused step on `stream`. Returns the CUDA launch error.
+cudaError_t launch_adamw(const AdamLaunch& a, cudaStream_t stream);
+
+cudaError_t launch_grad_stats(const void* grad, int grad_dtype, std::uint64_t n, float grad_scale,
+                              double* grad_sq_sum, int accumulate, float* workspace,
+                              int* nonfinite, cudaStream_t stream);
+
+// Grid geometry used for the device (cached per device).
+struct Geometry {
+    int sm_count = 0;
+    int ctas_per_sm = 0;
+};
+Geometry geometry(int device);
+
+} // namespace fy

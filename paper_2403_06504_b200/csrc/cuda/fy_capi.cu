@@ -1,0 +1,199 @@
+// C ABI of the B200 optimizer path (include/fuyou/fy_adam.h).
+// Error handling mirrors the reference C ABI (proj/src/capi.cpp:19-51):
+// thread-local last error, every body wrapped so no exception escapes.
+
+#include "fuyou/fy_adam.h"
+
+#include "adamw_kernels.cuh"
+#include "pipeline.cuh"
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+namespace {
+
+thread_local std::string g_fy_error;
+
+fy_status fail(fy_status code, const std::string& msg) {
+    g_fy_error = msg;
+    return code;
+}
+
+template <typename Fn>
+fy_status guard(Fn&& fn) {
+    try {
+        return fn();
+    } catch (const fy::ArgError& e) {
+        return fail(FY_ERR_CONFIG, e.what());
+    } catch (const fy::DeviceError& e) {
+        return fail(FY_ERR_DEVICE, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(FY_ERR_INFEASIBLE, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(FY_ERR_INTERNAL, e.what());
+    } catch (...) {
+        return fail(FY_ERR_INTERNAL, "unknown error");
+    }
+}
+
+bool valid_grad_dtype(int d) { return d == FY_BF16 || d == FY_FP16 || d == FY_FP32; }
+bool valid_param_dtype(int d) { return d == FY_BF16 || d == FY_FP16; }
+
+} // namespace
+
+struct fy_pipeline {
+    explicit fy_pipeline(const fy_pipeline_config& c) : impl(c) {}
+    fy::ChunkPipeline impl;
+};
+
+extern "C" {
+
+const char* fy_version(void) { return "0.1.0-b200"; }
+
+const char* fy_last_error(void) { return g_fy_error.c_str(); }
+
+uint32_t fy_adamw_workspace_floats(void) { return fy::kWorkspaceFloats; }
+
+fy_status fy_adamw_chunk(const fy_adamw_args* a, void* stream) {
+    if (!a) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        if (a->n > 0 && (!a->master || !a->exp_avg || !a->exp_avg_sq || !a->grad))
+            return fail(FY_ERR_CONFIG, "null argument");
+        if (!valid_grad_dtype(a->grad_dtype)) return fail(FY_ERR_CONFIG, "bad grad_dtype");
+        if (a->param_out && !valid_param_dtype(a->param_dtype))
+            return fail(FY_ERR_CONFIG, "param_dtype must be bf16 or fp16");
+        if (a->param_out && a->param_out == a->grad && a->grad_dtype == FY_FP32)
+            return fail(FY_ERR_CONFIG, "param_out may alias grad only for 16-bit grads");
+        if (a->grad_sq_sum && !a->workspace)
+            return fail(FY_ERR_CONFIG, "grad_sq_sum requires workspace");
+        if (a->hp.step == 0) return fail(FY_ERR_CONFIG, "step must be >= 1");
+        fy::AdamLaunch l{};
+        l.master = a->master;
+        l.m = a->exp_avg;
+        l.v = a->exp_avg_sq;
+        l.grad = a->grad;
+        l.grad_dtype = a->grad_dtype;
+        l.param = a->param_out;
+        l.param_dtype = a->param_dtype;
+        l.n = a->n;
+        l.s = fy::make_scalars(a->hp.lr, a->hp.beta1, a->hp.beta2, a->hp.eps, a->hp.weight_decay,
+                               a->hp.step, a->hp.adamw_mode, a->hp.bias_correction,
+                               a->hp.grad_scale);
+        l.grad_sq_sum = a->grad_sq_sum;
+        l.accumulate_sq = a->accumulate_sq;
+        l.workspace = a->workspace;
+        l.nonfinite = a->nonfinite_flag;
+        fy::check_cuda(fy::launch_adamw(l, static_cast<cudaStream_t>(stream)), "fy_adamw_chunk");
+        return FY_OK;
+    });
+}
+
+fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad_scale,
+                        double* grad_sq_sum, int accumulate_sq, float* workspace,
+                        int* nonfinite_flag, void* stream) {
+    if (n > 0 && !grad) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        if (!valid_grad_dtype(grad_dtype)) return fail(FY_ERR_CONFIG, "bad grad_dtype");
+        if (grad_sq_sum && !workspace) return fail(FY_ERR_CONFIG, "grad_sq_sum requires workspace");
+        fy::check_cuda(fy::launch_grad_stats(grad, grad_dtype, n, grad_scale, grad_sq_sum,
+                                             accumulate_sq, workspace, nonfinite_flag,
+                                             static_cast<cudaStream_t>(stream)),
+                       "fy_grad_stats");
+        return FY_OK;
+    });
+}
+
+fy_status fy_device_info(int device, int* sm_count, int* ctas_per_sm, int* threads_per_cta) {
+    if (!sm_count || !ctas_per_sm || !threads_per_cta) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        int ndev = 0;
+        fy::check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) return fail(FY_ERR_CONFIG, "no such device");
+        int prev = 0;
+        fy::check_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+        fy::check_cuda(cudaSetDevice(device), "cudaSetDevice");
+        const fy::Geometry g = fy::geometry(device);
+        cudaSetDevice(prev);
+        *sm_count = g.sm_count;
+        *ctas_per_sm = g.ctas_per_sm;
+        *threads_per_cta = fy::kThreads;
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_range(uint64_t n, uint32_t world, uint32_t rank, uint32_t align,
+                         uint64_t* offset, uint64_t* count) {
+    if (!offset || !count) return fail(FY_ERR_CONFIG, "null argument");
+    if (world == 0 || rank >= world) return fail(FY_ERR_CONFIG, "rank out of range");
+    if (align == 0) align = 1;
+    // Equal slices rounded up to `align`; the tail rank takes the remainder
+    // (possibly empty when n is small).
+    const uint64_t per = (n + world - 1) / world;
+    const uint64_t slice = (per + align - 1) / align * align;
+    const uint64_t begin = std::min<uint64_t>(n, slice * rank);
+    const uint64_t end = std::min<uint64_t>(n, slice * (rank + 1ull));
+    *offset = begin;
+    *count = end - begin;
+    return FY_OK;
+}
+
+fy_status fy_pipeline_create(const fy_pipeline_config* cfg, fy_pipeline** out) {
+    if (!cfg || !out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        *out = new fy_pipeline(*cfg);
+        return FY_OK;
+    });
+}
+
+void fy_pipeline_destroy(fy_pipeline* p) { delete p; }
+
+fy_status fy_pipeline_step(fy_pipeline* p, const fy_chunk* chunks, uint32_t count,
+                           const fy_adam_hparams* hp, int want_grad_norm) {
+    if (!p || !chunks || !hp) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        if (hp->step == 0) return fail(FY_ERR_CONFIG, "step must be >= 1");
+        p->impl.step(chunks, count, *hp, want_grad_norm != 0);
+        return FY_OK;
+    });
+}
+
+fy_status fy_pipeline_wait(fy_pipeline* p, double* grad_sq_sum, int* nonfinite) {
+    if (!p) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        p->impl.wait(grad_sq_sum, nonfinite);
+        return FY_OK;
+    });
+}
+
+fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32_t count,
+                              uint64_t* step_ns) {
+    if (!p || (!out && count > 0)) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        p->impl.timings(out, count, step_ns);
+        return FY_OK;
+    });
+}
+
+fy_status fy_host_alloc(uint64_t bytes, void** out) {
+    if (!out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        void* p = nullptr;
+        const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+        if (e == cudaErrorMemoryAllocation)
+            return fail(FY_ERR_INFEASIBLE, "pinned host allocation of " + std::to_string(bytes) +
+                                               " bytes failed");
+        fy::check_cuda(e, "cudaHostAlloc");
+        *out = p;
+        return FY_OK;
+    });
+}
+
+fy_status fy_host_free(void* p) {
+    return guard([&] {
+        if (p) fy::check_cuda(cudaFreeHost(p), "cudaFreeHost");
+        return FY_OK;
+    });
+}
+
+} // extern "C"

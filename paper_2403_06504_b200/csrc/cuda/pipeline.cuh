@@ -1,0 +1,80 @@
+// Chunk pipeline for the streamed (out-of-core) optimizer step.
+#pragma once
+
+#include "adamw_kernels.cuh"
+#include "fuyou/fy_adam.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace fy {
+
+// Raised for CUDA failures; the C ABI maps it to FY_ERR_DEVICE.
+struct DeviceError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ArgError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+
+// Device staging for one chunk in flight: [master | m | v] (12n B), plus a
+// gradient area (host-sourced grads) and a param area (downcast output).
+struct Slot {
+    unsigned char* states = nullptr;
+    void* grad = nullptr;
+    void* param = nullptr;
+};
+
+class ChunkPipeline {
+public:
+    explicit ChunkPipeline(const fy_pipeline_config& cfg);
+    ~ChunkPipeline();
+    ChunkPipeline(const ChunkPipeline&) = delete;
+    ChunkPipeline& operator=(const ChunkPipeline&) = delete;
+
+    void step(const fy_chunk* chunks, std::uint32_t count, const fy_adam_hparams& hp,
+              bool want_norm);
+    void wait(double* grad_sq_sum, int* nonfinite);
+    void timings(fy_chunk_timing* out, std::uint32_t count, std::uint64_t* step_ns) const;
+
+    cudaStream_t h2d_stream() const { return h2d_; }
+    cudaStream_t d2h_stream() const { return d2h_; }
+    cudaStream_t compute_stream() const { return opt_; }
+
+private:
+    enum Ev { kH2dStart, kH2dEnd, kUpdStart, kUpdEnd, kD2hStart, kD2hEnd, kEvPerChunk };
+    cudaEvent_t ev(std::uint32_t chunk, int which) const { return events_[chunk * kEvPerChunk + which]; }
+    void ensure_events(std::uint32_t count);
+    void issue_h2d(std::uint32_t i);
+    void issue_update(std::uint32_t i);
+    void issue_d2h(std::uint32_t i);
+
+    fy_pipeline_config cfg_{};
+    int grad_bytes_ = 2;
+    int param_bytes_ = 2;
+    cudaStream_t h2d_ = nullptr, d2h_ = nullptr, opt_ = nullptr;
+    std::vector<Slot> slots_;
+    std::vector<cudaEvent_t> events_;
+    cudaEvent_t step_start_ = nullptr;
+    cudaEvent_t step_end_ = nullptr;
+    float* workspace_ = nullptr;
+    double* d_norm_ = nullptr;
+    int* d_nonfinite_ = nullptr;
+    double* h_norm_ = nullptr;
+    int* h_nonfinite_ = nullptr;
+    bool want_norm_ = false;
+    bool pending_ = false;
+    bool have_prev_ = false;
+    std::uint32_t last_count_ = 0;
+    // Current step's inputs (valid during step()).
+    const fy_chunk* chunks_ = nullptr;
+    AdamScalars scalars_{};
+};
+
+} // namespace fy

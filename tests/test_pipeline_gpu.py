@@ -1,0 +1,91 @@
+"""GPU parity + ordering of the streamed (out-of-core) optimizer step
+(fy_pipeline_*): host-resident [master|m|v] per chunk, H2D -> fused Adam ->
+D2H, against the CPU oracle; and the executed timeline against the
+reference's optimizer-block dependencies (task_graph.cpp:453-503): read gate
+depth 2, update after its read, write-back after its update, slot reuse
+after the previous write-back."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits_equal(x, y):
+    return bool(np.array_equal(x.view(np.uint32), y.view(np.uint32)))
+
+
+def _make_chunks(sizes, seed, dev, grads_on_host):
+    chunks, ref = [], []
+    for k, n in enumerate(sizes):
+        rng = np.random.default_rng(20240817 + seed + k)
+        st = np.empty(3 * n, np.float32)
+        st[:n] = rng.normal(0, 0.02, n)
+        st[n:2 * n] = rng.normal(0, 1e-3, n)
+        st[2 * n:] = rng.normal(0, 1e-3, n) ** 2
+        g = torch.from_numpy(rng.normal(0, 1e-3, n).astype(np.float32)).to(torch.bfloat16)
+        h_states = torch.from_numpy(st.copy()).pin_memory()
+        h_param = torch.zeros(n, dtype=torch.bfloat16).pin_memory()
+        grad = g.pin_memory() if grads_on_host else g.to(dev)
+        chunks.append(dict(n=n, h_states_t=h_states, grad_t=grad, h_param_t=h_param))
+        ref.append(dict(states=st, grad=g.view(torch.int16).numpy().view(np.uint16).copy()))
+    return chunks, ref
+
+
+def _desc(chunks):
+    return [dict(n=c["n"], h_states=c["h_states_t"].data_ptr(), grad=c["grad_t"].data_ptr(),
+                 h_param=c["h_param_t"].data_ptr()) for c in chunks]
+
+
+@pytest.mark.parametrize("grads_on_host,slots", [(False, 3), (True, 2), (False, 4)])
+def test_pipeline_matches_oracle(cuda_dev, grads_on_host, slots):
+    from paper_2403_06504_b200 import optim as F
+    sizes = [1 << 20, (1 << 20) + 3, 4099, 777777, 1 << 19, 8]
+    chunks, ref = _make_chunks(sizes, 1, cuda_dev, grads_on_host)
+    pipe = F.ChunkPipeline(max(sizes), slots=slots, grads_on_host=grads_on_host)
+    sq_total = 0.0
+    for step in (10, 11):
+        hp = F.Hparams(step=step)
+        pipe.step(_desc(chunks), hp, want_grad_norm=True)
+        sq, bad = pipe.wait()
+        assert bad == 0
+        sc = O.scalars(step=step)
+        sq_ref = 0.0
+        for r in ref:
+            n = r["grad"].size
+            st = r["states"]
+            r["param"] = np.zeros(n, np.uint16)
+            mst, mm, vv = st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()
+            s, _ = O.adamw_step(mst, mm, vv, r["grad"], O.BF16, sc, param_out=r["param"])
+            sq_ref += s
+            r["states"] = np.concatenate([mst, mm, vv])
+        assert abs(sq - sq_ref) <= 1e-5 * sq_ref
+        for c, r in zip(chunks, ref):
+            assert _bits_equal(c["h_states_t"].numpy(), r["states"])
+            assert np.array_equal(c["h_param_t"].view(torch.int16).numpy().view(np.uint16),
+                                  r["param"])
+        tim, total = pipe.timings(len(sizes))
+        assert total > 0
+        for i, t in enumerate(tim):
+            assert t["upd"][0] >= t["h2d"][1], "update before its state read"
+            assert t["d2h"][0] >= t["upd"][1], "write-back before its update"
+            if i >= 2:
+                assert t["h2d"][0] >= tim[i - 2]["upd"][1], "read gate (depth 2) violated"
+            if i >= slots:
+                assert t["h2d"][0] >= tim[i - slots]["d2h"][1], "slot reused before write-back"
+    pipe.close()
+
+
+def test_pipeline_rejects_bad_args(cuda_dev):
+    from paper_2403_06504_b200 import optim as F
+    from paper_2403_06504_b200._lib import FyError
+    pipe = F.ChunkPipeline(1024, slots=2)
+    with pytest.raises(FyError):
+        pipe.step([dict(n=4096, h_states=1, grad=1, h_param=1)], F.Hparams())
+    with pytest.raises(FyError):
+        pipe.wait()
+    pipe.close()
+    with pytest.raises(FyError):
+        F.ChunkPipeline(1024, slots=1)
