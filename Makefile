@@ -49,10 +49,26 @@ build/offsim_dump: tests/parity/offsim_dump.cpp build/liboffsim_core.a
 oracle:
 	$(MAKE) -C oracle all
 
+# The reference's own unit suites (unmodified, from /root/reference) built
+# against THIS repo's headers + core / C ABI through the doctest shim —
+# only where the reference sources exist (build container).
+REF      ?= /root/reference/proj
+REF_UNIT := $(REF)/tests/main.cpp $(addprefix $(REF)/tests/test_,$(addsuffix .cpp,workload hardware cost_model planner sim capacity scenario))
+reftests: build/ref_unit_tests_on_b200 build/ref_capi_tests_on_b200 build/ref_acceptance_on_b200
+
+build/ref_unit_tests_on_b200: $(REF_UNIT) build/liboffsim_core.a tests/parity/doctest_shim/doctest.h
+	$(CXX) $(CXXFLAGS) -Itests/parity/doctest_shim $(REF_UNIT) build/liboffsim_core.a -pthread -o $@
+
+build/ref_capi_tests_on_b200: $(REF)/tests/test_capi.cpp $(LIBDIR)/liboffsim.so tests/parity/doctest_shim/doctest.h
+	$(CXX) $(CXXFLAGS) -Itests/parity/doctest_shim $< -L$(LIBDIR) -l:liboffsim.so.0 -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)' -o $@
+
+build/ref_acceptance_on_b200: $(REF)/tests/acceptance/acceptance_main.cpp build/liboffsim_core.a
+	$(CXX) $(CXXFLAGS) $< build/liboffsim_core.a -pthread -o $@
+
 ref:
 	$(MAKE) -C oracle ref
 
 clean:
 	rm -rf build $(LIBDIR)
 
-.PHONY: all oracle ref clean
+.PHONY: all oracle ref reftests clean

@@ -183,6 +183,17 @@ fy_status fy_pipeline_wait(fy_pipeline* p, double* grad_sq_sum, int* nonfinite);
 fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32_t count,
                               uint64_t* step_ns);
 
+/* ------------------------------------------------------------------ */
+/* Whole-iteration execution of a scenario's task graph on the GPU with
+ * caller-owned optimizer states (one fy_chunk per transformer block, n =
+ * 12h^2; h_states pinned host [master|m|v], h_param pinned host bf16 output,
+ * grad a device bf16 pointer). Same semantics as offsim_execute (see
+ * include/offsim/exec.hpp); the summary JSON is library-allocated (free it
+ * with offsim_string_free). Errors are reported through offsim_last_error.
+ * chunk_count 0 = synthetic states. */
+fy_status fy_graph_execute(const char* scenario_json, const char* exec_opts_json,
+                           const fy_chunk* chunks, uint32_t chunk_count, char** summary_json_out);
+
 /* Pinned host allocation helpers (cudaHostAlloc, portable). */
 fy_status fy_host_alloc(uint64_t bytes, void** out);
 fy_status fy_host_free(void* p);

@@ -1,0 +1,124 @@
+// B200 executor — the real counterpart of simulate().
+//
+//   SimTrace simulate(const TaskGraph&, const HardwareConfig&)   (reference)
+//   ExecReport execute(model, hw, plan, variant, ExecOptions)     (this)
+//
+// The reference prices a CPU optimizer and an SSD array; on B200 the Adam
+// step runs on the GPU (fused kernel), so the executor first rewrites the
+// reference task graph with a *tier map* (map_graph_for_b200) and then runs
+// every task of the mapped graph on real engines:
+//
+//   reference task                      B200 operation (lane in the trace)
+//   opt update gK   (cpu_compute)       fused AdamW kernel, optimizer stream
+//                                       (cpu_compute lane = "optimizer")
+//   + inserted opt state_h2d gK         H2D of [master|m|v] (link_c2g)
+//   + inserted opt state_d2h gK         D2H of the updated states (link_g2c)
+//   + inserted opt param_d2h gK         D2H of the bf16 params (link_g2c)
+//   bwd grad_g2c / grad_c2s / grad_s2c  no bytes: grads stay in HBM (A5)
+//   *_s2c / *_c2s on link_ssd           tier "file": pread/pwrite (O_DIRECT)
+//                                       of real files; tier "host": no bytes
+//                                       (the pinned host DRAM *is* the tier)
+//   p_c2g / ckpt_c2g / act_c2g          H2D copy engine (link_c2g)
+//   act_g2c / ckpt_g2c                  D2H copy engine (link_g2c)
+//   fwd/bwd compute, recompute          synthetic compute: a timed kernel of
+//                                       work / compute_rate seconds
+//
+// Every inserted task carries explicit dependencies, so the mapped graph is
+// an ordinary TaskGraph: the executed trace is validated by the UNCHANGED
+// check_trace_invariants against a HardwareConfig of measured B200 rates,
+// and the report lists reference-graph bytes and physically moved bytes
+// separately. Issue order on each engine follows simulate() of the mapped
+// graph, so real execution replays the planned schedule.
+#pragma once
+
+#include "offsim/hardware.hpp"
+#include "offsim/planner.hpp"
+#include "offsim/sim.hpp"
+#include "offsim/workload.hpp"
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+namespace offsim {
+
+enum class StateTier : std::uint8_t { host, file };
+const char* to_string(StateTier t);
+
+struct AdamHyper {
+    float lr = 1e-4f;
+    float beta1 = 0.9f;
+    float beta2 = 0.95f;
+    float eps = 1e-8f;
+    float weight_decay = 0.1f;
+    std::uint64_t step = 10;
+    bool adamw_mode = true;
+    bool bias_correction = true;
+    float grad_scale = 1.0f;
+};
+
+struct ExecOptions {
+    int device = 0;
+    StateTier tier = StateTier::host;
+    std::string file_dir = "/tmp/offsim_b200";
+    bool direct_io = true;          // O_DIRECT for the file tier
+    double compute_rate = 0.0;      // FLOP/s of synthetic compute (0: hw.gpu_tput)
+    std::uint32_t state_slots = 3;  // device staging slots for optimizer groups
+    AdamHyper adam;
+    std::uint64_t seed = 0;         // synthetic states / grads / activations
+    bool verify_swaps = true;       // checksum every restored activation
+};
+
+// Caller-provided optimizer states for chunk (block) k: pinned host
+// [master | m | v] (12n B) and the bf16 param output (2n B). When absent the
+// executor allocates and seeds them itself.
+struct ChunkBuffers {
+    void* host_states = nullptr;
+    void* host_params = nullptr;
+    const void* device_grads = nullptr; // bf16 [n]; synthetic when null
+};
+
+// Graph rewrite only (no device needed): inserted hop tasks, zeroed byte
+// counts for transfers that do not physically happen on B200 under `tier`.
+// The m-th optimizer group (processing order) stages its states in device
+// slot m % state_slots; the slot-reuse edge is part of the mapped graph.
+TaskGraph map_graph_for_b200(const TaskGraph& graph, StateTier tier,
+                             std::uint32_t state_slots = 3);
+
+// HardwareConfig describing the B200 box for the mapped graph's DES order
+// and invariant checks (measured rates override the preset's).
+struct MeasuredRates {
+    double h2d_bps = 0.0;
+    double d2h_bps = 0.0;
+    double file_read_bps = 0.0;
+    double file_write_bps = 0.0;
+    double optimizer_params_per_s = 0.0;
+    double compute_flops = 0.0;
+    std::uint64_t gpu_mem = 0;
+    std::uint64_t cpu_mem = 0;
+};
+HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRates& r);
+
+struct ExecReport {
+    TaskGraph graph;        // the mapped graph that ran
+    SimTrace trace;         // real timings (CUDA events), same type as simulate()
+    SimTrace planned;       // simulate() of the mapped graph on `hw_exec`
+    InvariantReport invariants;
+    HardwareConfig hw_exec;
+    std::map<std::string, double> reference_bytes; // "<lane>/<payload>" of the input graph
+    std::map<std::string, double> physical_bytes;  // "h2d|d2h|file_read|file_write/<payload>"
+    double grad_sq_sum = 0.0;
+    int nonfinite = 0;
+    std::uint64_t swap_checks = 0;     // restored buffers verified
+    std::uint64_t swap_mismatches = 0; // must be 0
+    std::uint32_t kernel_launches = 0;
+};
+
+ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const SwapPlan& plan,
+                   ScheduleVariant variant, const ExecOptions& options,
+                   const std::vector<ChunkBuffers>* chunks = nullptr);
+
+std::string exec_summary_json(const ExecReport& r);
+
+} // namespace offsim

@@ -30,3 +30,16 @@ $(OUT)/offsim_dump_ref: $(TESTS)/parity/offsim_dump.cpp $(OUT)/liboffsim_core.a
 	$(CXX) $(CXXFLAGS) $< $(OUT)/liboffsim_core.a -pthread -o $@
 
 .PHONY: all
+
+# Reference unit suites (unmodified sources) on the doctest shim, linked
+# against the reference core: calibrates the shim (must pass 100%).
+UNIT := $(REF)/tests/main.cpp $(addprefix $(REF)/tests/test_,$(addsuffix .cpp,workload hardware cost_model planner sim capacity scenario))
+SHIM := -I$(TESTS)/parity/doctest_shim
+
+all: $(OUT)/ref_unit_tests $(OUT)/ref_capi_tests
+
+$(OUT)/ref_unit_tests: $(UNIT) $(OUT)/liboffsim_core.a $(TESTS)/parity/doctest_shim/doctest.h
+	$(CXX) $(CXXFLAGS) $(SHIM) $(UNIT) $(OUT)/liboffsim_core.a -pthread -o $@
+
+$(OUT)/ref_capi_tests: $(REF)/tests/test_capi.cpp $(OUT)/liboffsim_ref.so $(TESTS)/parity/doctest_shim/doctest.h
+	$(CXX) $(CXXFLAGS) $(SHIM) $< -L$(OUT) -loffsim_ref -Wl,-rpath,'$$ORIGIN' -o $@

@@ -1,0 +1,257 @@
+// B200 execution entry points of the C ABI:
+//   offsim_execute      (include/offsim/offsim_c.h) scenario -> real run
+//   fy_graph_execute    (include/fuyou/fy_adam.h)   same, with caller-owned
+//                                                   per-chunk state buffers
+// plus the JSON codecs of ExecOptions and ExecReport. A {"dry_run": true}
+// option plans, maps and simulates without touching a GPU (CPU tests).
+
+#include "capi_internal.hpp"
+
+#include "fuyou/fy_adam.h"
+#include "offsim/exec.hpp"
+#include "offsim/runner.hpp"
+
+#include <json.hpp>
+
+#include <set>
+
+namespace offsim {
+
+using json = nlohmann::ordered_json;
+
+namespace {
+
+struct ParsedOptions {
+    ExecOptions exec;
+    bool dry_run = false;
+    std::string variant; // optional override
+};
+
+ParsedOptions parse_options(const char* text) {
+    ParsedOptions out;
+    if (!text || !*text) return out;
+    json doc;
+    try {
+        doc = json::parse(text);
+    } catch (const json::parse_error& e) {
+        throw ConfigError(std::string("exec options parse error: ") + e.what());
+    }
+    if (!doc.is_object()) throw ConfigError("exec options must be an object");
+    static const std::set<std::string> keys = {"device", "tier", "file_dir", "direct_io",
+                                               "compute_rate", "state_slots", "seed",
+                                               "verify_swaps", "adam", "dry_run", "variant"};
+    for (const auto& it : doc.items())
+        if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
+    try {
+        ExecOptions& o = out.exec;
+        o.device = doc.value("device", o.device);
+        const std::string tier = doc.value("tier", std::string("host"));
+        if (tier == "host") o.tier = StateTier::host;
+        else if (tier == "file") o.tier = StateTier::file;
+        else throw ConfigError("exec options: tier must be 'host' or 'file'");
+        o.file_dir = doc.value("file_dir", o.file_dir);
+        o.direct_io = doc.value("direct_io", o.direct_io);
+        o.compute_rate = doc.value("compute_rate", o.compute_rate);
+        o.state_slots = doc.value("state_slots", o.state_slots);
+        o.seed = doc.value("seed", o.seed);
+        o.verify_swaps = doc.value("verify_swaps", o.verify_swaps);
+        out.dry_run = doc.value("dry_run", false);
+        out.variant = doc.value("variant", std::string());
+        if (doc.contains("adam")) {
+            const json& a = doc.at("adam");
+            static const std::set<std::string> akeys = {"lr", "beta1", "beta2", "eps", "weight_decay",
+                                                        "step", "adamw_mode", "bias_correction",
+                                                        "grad_scale"};
+            for (const auto& it : a.items())
+                if (!akeys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options.adam");
+            AdamHyper& h = o.adam;
+            h.lr = a.value("lr", h.lr);
+            h.beta1 = a.value("beta1", h.beta1);
+            h.beta2 = a.value("beta2", h.beta2);
+            h.eps = a.value("eps", h.eps);
+            h.weight_decay = a.value("weight_decay", h.weight_decay);
+            h.step = a.value("step", h.step);
+            h.adamw_mode = a.value("adamw_mode", h.adamw_mode);
+            h.bias_correction = a.value("bias_correction", h.bias_correction);
+            h.grad_scale = a.value("grad_scale", h.grad_scale);
+            if (h.step < 1) throw ConfigError("exec options: adam.step must be >= 1");
+        }
+        if (o.state_slots < 2) throw ConfigError("exec options: state_slots must be >= 2");
+    } catch (const json::exception& e) {
+        throw ConfigError(std::string("exec options: bad value: ") + e.what());
+    }
+    return out;
+}
+
+json bytes_json(const std::map<std::string, double>& m) {
+    json j = json::object();
+    for (const auto& [k, v] : m) j[k] = v;
+    return j;
+}
+
+json trace_stats(const SimTrace& t) {
+    json busy = json::object();
+    for (const auto& [lane, ns] : t.busy_ns) busy[to_string(lane)] = static_cast<double>(ns) * 1e-9;
+    json peaks = json::object();
+    for (const auto& [pool, b] : t.peak_mem) peaks[to_string(pool)] = b;
+    return json{{"makespan_s", t.makespan_s()}, {"busy_s", busy}, {"peak_mem_bytes", peaks}};
+}
+
+// Per optimizer group: real timings of its hops (state_h2d -> update ->
+// state_d2h/param_d2h), the evidence for overlap with backward.
+json optimizer_json(const ExecReport& r) {
+    double upd_ns = 0, n_upd = 0, params = 0;
+    std::uint64_t first = ~0ull, last = 0;
+    std::map<std::uint32_t, const TraceEvent*> ev;
+    for (const TraceEvent& e : r.trace.events) ev[e.task_id] = &e;
+    for (const Task& t : r.graph.tasks) {
+        if (t.kind != TaskKind::optimizer_update) continue;
+        const TraceEvent* e = ev.at(t.id);
+        upd_ns += static_cast<double>(e->end_ns - e->start_ns);
+        n_upd += 1;
+        params += t.work;
+        first = std::min(first, e->start_ns);
+        last = std::max(last, e->end_ns);
+    }
+    return json{{"groups", n_upd},
+                {"params", params},
+                {"kernel_time_s", upd_ns * 1e-9},
+                {"kernel_params_per_s", upd_ns > 0 ? params / (upd_ns * 1e-9) : 0.0},
+                {"window_s", last > first ? static_cast<double>(last - first) * 1e-9 : 0.0},
+                {"grad_sq_sum", r.grad_sq_sum},
+                {"nonfinite", r.nonfinite}};
+}
+
+} // namespace
+
+std::string exec_summary_json(const ExecReport& r) {
+    json checks = json::array();
+    for (const auto& e : r.invariants.entries)
+        checks.push_back(json{{"name", e.name}, {"pass", e.pass}, {"detail", e.detail}});
+    const HardwareConfig& h = r.hw_exec;
+    const json doc = {
+        {"schema_version", 1},
+        {"command", "execute"},
+        {"variant", to_string(r.graph.header.variant)},
+        {"checkpoint_location", r.graph.header.checkpoint_location},
+        {"task_count", r.graph.tasks.size()},
+        {"hw_exec", json{{"bw_gpu", h.bw_gpu}, {"bw_s2c", h.bw_s2c}, {"bw_c2s", h.bw_c2s},
+                         {"cpu_opt_tput", h.cpu_opt_tput}, {"gpu_tput", h.gpu_tput},
+                         {"gpu_mem", h.gpu_mem}, {"cpu_mem", h.cpu_mem}}},
+        {"executed", trace_stats(r.trace)},
+        {"planned", trace_stats(r.planned)},
+        {"optimizer", optimizer_json(r)},
+        {"reference_bytes", bytes_json(r.reference_bytes)},
+        {"physical_bytes", bytes_json(r.physical_bytes)},
+        {"swap_checks", r.swap_checks},
+        {"swap_mismatches", r.swap_mismatches},
+        {"kernel_launches", r.kernel_launches},
+        {"invariants", checks},
+        {"all_invariants_pass", r.invariants.all_pass && r.swap_mismatches == 0},
+    };
+    return doc.dump(2) + "\n";
+}
+
+namespace {
+
+// Dry run: the mapped graph and its DES on nominal B200 rates (no GPU).
+std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVariant v) {
+    const SwapPlan plan = plan_for_scenario(s);
+    const TaskGraph ref = build_schedule(s.model, s.hardware, plan, v);
+    const TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots);
+    MeasuredRates nominal;
+    nominal.h2d_bps = nominal.d2h_bps = 55e9;
+    nominal.file_read_bps = nominal.file_write_bps = po.exec.tier == StateTier::file ? 2e9 : 0.0;
+    nominal.optimizer_params_per_s = 2.1e11;
+    nominal.compute_flops = po.exec.compute_rate > 0 ? po.exec.compute_rate : s.hardware.gpu_tput;
+    nominal.gpu_mem = 180ull * 1000 * 1000 * 1000;
+    nominal.cpu_mem = 2000ull * 1000 * 1000 * 1000;
+    const HardwareConfig hw = b200_hardware(s.hardware, nominal);
+    const SimTrace tr = simulate(mapped, hw);
+    const InvariantReport inv = check_trace_invariants(mapped, tr, hw);
+    std::map<std::string, double> ref_bytes, mapped_bytes;
+    for (const Task& t : ref.tasks)
+        if (t.kind == TaskKind::transfer)
+            ref_bytes[std::string(to_string(t.resource)) + "/" + to_string(t.payload)] += t.work;
+    json inserted = json::array();
+    for (const Task& t : mapped.tasks) {
+        if (t.kind == TaskKind::transfer)
+            mapped_bytes[std::string(to_string(t.resource)) + "/" + to_string(t.payload)] += t.work;
+        if (t.name.find("_h2d ") != std::string::npos || t.name.find("_d2h ") != std::string::npos)
+            inserted.push_back(t.name);
+    }
+    json checks = json::array();
+    for (const auto& e : inv.entries)
+        checks.push_back(json{{"name", e.name}, {"pass", e.pass}, {"detail", e.detail}});
+    const json doc = {{"schema_version", 1},
+                      {"command", "execute"},
+                      {"dry_run", true},
+                      {"variant", to_string(v)},
+                      {"reference_task_count", ref.tasks.size()},
+                      {"task_count", mapped.tasks.size()},
+                      {"inserted_tasks", inserted},
+                      {"reference_bytes", bytes_json(ref_bytes)},
+                      {"mapped_bytes", bytes_json(mapped_bytes)},
+                      {"planned", trace_stats(tr)},
+                      {"invariants", checks},
+                      {"all_invariants_pass", inv.all_pass}};
+    return doc.dump(2) + "\n";
+}
+
+offsim_status run_exec(const Scenario& s, const char* opts_json,
+                       const std::vector<ChunkBuffers>* chunks, char** summary_out,
+                       char** trace_out) {
+    const ParsedOptions po = parse_options(opts_json);
+    const ScheduleVariant v =
+        po.variant.empty() ? s.variant : schedule_variant_from_string(po.variant);
+    Scenario sv = s;
+    sv.variant = v;
+    if (po.dry_run) {
+        *summary_out = capi::copy_out(dry_run_json(sv, po, v));
+        if (trace_out) *trace_out = nullptr;
+        return OFFSIM_OK;
+    }
+    const SwapPlan plan = plan_for_scenario(sv);
+    const ExecReport rep = execute(sv.model, sv.hardware, plan, v, po.exec, chunks);
+    const std::string summary = exec_summary_json(rep);
+    *summary_out = capi::copy_out(summary);
+    if (trace_out) *trace_out = capi::copy_out(to_chrome_trace_json(rep.graph, rep.trace));
+    if (!rep.invariants.all_pass || rep.swap_mismatches != 0)
+        return capi::fail(OFFSIM_ERR_INVARIANT, "executed trace failed its checks; see summary");
+    return OFFSIM_OK;
+}
+
+} // namespace
+
+} // namespace offsim
+
+extern "C" {
+
+offsim_status offsim_execute(const offsim_scenario* s, const char* exec_opts_json,
+                             char** summary_json_out, char** trace_json_out) {
+    if (!s || !summary_json_out) return offsim::capi::fail(OFFSIM_ERR_CONFIG, "null argument");
+    return offsim::capi::guarded([&] {
+        return offsim::run_exec(s->scenario, exec_opts_json, nullptr, summary_json_out, trace_json_out);
+    });
+}
+
+fy_status fy_graph_execute(const char* scenario_json, const char* exec_opts_json,
+                           const fy_chunk* chunks, uint32_t chunk_count, char** summary_json_out) {
+    if (!scenario_json || !summary_json_out || (chunk_count && !chunks))
+        return static_cast<fy_status>(offsim::capi::fail(OFFSIM_ERR_CONFIG, "null argument"));
+    const offsim_status st = offsim::capi::guarded([&] {
+        const offsim::Scenario sc = offsim::load_scenario(scenario_json);
+        std::vector<offsim::ChunkBuffers> bufs;
+        for (uint32_t k = 0; k < chunk_count; ++k) {
+            if (chunks[k].n != 12ull * sc.model.hidden_dim * sc.model.hidden_dim)
+                throw offsim::ConfigError("fy_graph_execute: chunk " + std::to_string(k) +
+                                          " size differs from 12*h^2");
+            bufs.push_back({chunks[k].h_states, chunks[k].h_param, chunks[k].grad});
+        }
+        return offsim::run_exec(sc, exec_opts_json, chunk_count ? &bufs : nullptr, summary_json_out,
+                                nullptr);
+    });
+    return static_cast<fy_status>(st);
+}
+
+} // extern "C"

@@ -1,0 +1,174 @@
+// Tier map: rewrites a reference TaskGraph into the graph the B200 executor
+// runs (see include/offsim/exec.hpp). Pure graph transformation — testable
+// without a GPU (tests/test_tier_map.py through offsim_execute's dry run).
+//
+// Rules (reference anchors are proj/src/task_graph.cpp lines):
+//  * optimizer on the GPU (opt update gK, :488-495): insert
+//      "opt state_h2d gK"  link_c2g, 12N B, after state_s2c, before update
+//      "opt state_d2h gK"  link_g2c, 12N B, after update, before state_c2s
+//      "opt param_d2h gK"  link_g2c,  2N B, after update, before param_c2s
+//    (and for serial/pipelined, "opt grad_h2d gK" link_c2g 2N B after
+//    grad_s2c: those variants stage gradients through the SSD by definition)
+//  * overlapped: grads never leave HBM — bwd grad_g2c (:442-445) moves 0 B
+//  * tier host: every link_ssd task moves 0 B (pinned host DRAM is the
+//    tier); tier file: link_ssd tasks are real file reads / writes
+//  * memory pools re-booked: grad / param bytes leave the GPU pool at
+//    param_d2h instead of grad_g2c; the update has no CPU-side effect;
+//    states occupy a GPU staging slot from state_h2d to state_d2h.
+
+#include "offsim/errors.hpp"
+#include "offsim/exec.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+namespace offsim {
+
+const char* to_string(StateTier t) { return t == StateTier::host ? "host" : "file"; }
+
+namespace {
+
+bool starts_with(const std::string& s, const char* p) { return s.rfind(p, 0) == 0; }
+
+// "opt update g7" -> "g7"
+std::string group_of(const std::string& name) { return name.substr(name.rfind(' ') + 1); }
+
+} // namespace
+
+TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t state_slots) {
+    if (state_slots < 2) throw ConfigError("executor: state_slots must be >= 2");
+    const bool overlapped = in.header.variant == ScheduleVariant::overlapped;
+    if (!overlapped && tier == StateTier::host)
+        throw ConfigError(std::string("variant '") + to_string(in.header.variant) +
+                          "' stages gradients through the SSD; execute it with tier=file");
+
+    TaskGraph out;
+    out.header = in.header;
+    out.initial_mem = in.initial_mem;
+    std::vector<std::uint32_t> remap(in.tasks.size());
+    // Per optimizer group: ids of the inserted hops (in the output graph).
+    std::map<std::string, std::uint32_t> h2d_of, d2h_of, pd2h_of, gh2d_of;
+    // Device staging slot of the m-th optimizer group is m % state_slots; its
+    // state_h2d waits for the state_d2h of group m - state_slots (the slot's
+    // previous user) — a physical constraint made explicit as a graph edge.
+    std::vector<std::uint32_t> d2h_in_order;
+
+    auto push = [&](Task t) {
+        t.id = static_cast<std::uint32_t>(out.tasks.size());
+        std::sort(t.deps.begin(), t.deps.end());
+        t.deps.erase(std::unique(t.deps.begin(), t.deps.end()), t.deps.end());
+        out.tasks.push_back(std::move(t));
+        return out.tasks.back().id;
+    };
+    auto hop = [&](const std::string& name, ResourceId lane, TransferDir dir, Payload p,
+                   double bytes, std::vector<std::uint32_t> deps, std::vector<MemEffect> fx) {
+        Task t;
+        t.name = name;
+        t.kind = TaskKind::transfer;
+        t.resource = lane;
+        t.dir = dir;
+        t.payload = p;
+        t.work = bytes;
+        t.deps = std::move(deps);
+        t.mem_effects = std::move(fx);
+        return push(std::move(t));
+    };
+
+    // Pass 1: block geometry from the reference's own tasks.
+    std::map<std::string, double> state_bytes, param_bytes;
+    for (const Task& t : in.tasks) {
+        if (starts_with(t.name, "opt state_s2c ")) state_bytes[group_of(t.name)] = t.work;
+        if (starts_with(t.name, "opt param_c2s ")) param_bytes[group_of(t.name)] = t.work;
+    }
+
+    for (const Task& src : in.tasks) {
+        Task t = src;
+        for (auto& d : t.deps) d = remap[d];
+        const std::string g = group_of(src.name);
+        const auto i64 = [](double b) { return static_cast<std::int64_t>(b); };
+
+        if (t.resource == ResourceId::link_ssd && tier == StateTier::host) t.work = 0.0;
+
+        if (starts_with(src.name, "bwd grad_g2c ") && overlapped) {
+            // gradients stay in HBM and feed the fused kernel directly
+            t.work = 0.0;
+            t.mem_effects.clear();
+        } else if (starts_with(src.name, "opt update ")) {
+            if (!overlapped) {
+                // grad_s2c landed the grads in CPU memory; bring them back
+                // to the device (real bytes, the variant's definition)
+                std::uint32_t gs = 0;
+                for (const std::uint32_t d : t.deps)
+                    if (starts_with(out.tasks[d].name, "opt grad_s2c ")) gs = d;
+                const double gb = param_bytes[g];
+                gh2d_of[g] = hop("opt grad_h2d " + g, ResourceId::link_c2g, TransferDir::c2g,
+                                 Payload::grads, gb, {gs},
+                                 {MemEffect{ResourceId::mem_gpu, i64(gb), true},
+                                  MemEffect{ResourceId::mem_cpu, -i64(gb), false}});
+                t.deps.push_back(gh2d_of[g]);
+            }
+            // the states go to a device staging slot first
+            std::uint32_t state_read = 0;
+            for (const std::uint32_t d : t.deps)
+                if (starts_with(out.tasks[d].name, "opt state_s2c ")) state_read = d;
+            const double sb = state_bytes[g];
+            std::vector<std::uint32_t> h2d_deps{state_read};
+            if (d2h_in_order.size() >= state_slots)
+                h2d_deps.push_back(d2h_in_order[d2h_in_order.size() - state_slots]);
+            h2d_of[g] = hop("opt state_h2d " + g, ResourceId::link_c2g, TransferDir::c2g,
+                            Payload::opt_states, sb, std::move(h2d_deps),
+                            {MemEffect{ResourceId::mem_gpu, i64(sb), true}});
+            t.deps.push_back(h2d_of[g]);
+            t.mem_effects.clear();
+            const std::uint32_t upd = push(std::move(t));
+            remap[src.id] = upd;
+            const double pb = param_bytes[g];
+            d2h_of[g] = hop("opt state_d2h " + g, ResourceId::link_g2c, TransferDir::g2c,
+                            Payload::opt_states, sb, {upd},
+                            {MemEffect{ResourceId::mem_gpu, -i64(sb), false}});
+            d2h_in_order.push_back(d2h_of[g]);
+            pd2h_of[g] = hop("opt param_d2h " + g, ResourceId::link_g2c, TransferDir::g2c,
+                             Payload::params, pb, {upd},
+                             {MemEffect{ResourceId::mem_cpu, i64(pb), true},
+                              MemEffect{ResourceId::mem_gpu, -i64(pb), false}});
+            continue;
+        } else if (starts_with(src.name, "opt state_c2s ")) {
+            t.deps.push_back(d2h_of.at(g));
+        } else if (starts_with(src.name, "opt param_c2s ")) {
+            t.deps.push_back(pd2h_of.at(g));
+        }
+        // serial / pipelined bwd grad_g2c stays a real D2H of the grads
+        remap[src.id] = push(std::move(t));
+    }
+    if (in.header.variant == ScheduleVariant::serial) {
+        // keep the serial variant fully chained, inserted hops included
+        // (task_graph.cpp:92 chains every task to its predecessor)
+        for (Task& t : out.tasks)
+            if (t.id > 0 && std::find(t.deps.begin(), t.deps.end(), t.id - 1) == t.deps.end()) {
+                t.deps.push_back(t.id - 1);
+                std::sort(t.deps.begin(), t.deps.end());
+            }
+    }
+    return out;
+}
+
+HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRates& r) {
+    // Rates are upper bounds of what the engines delivered (measured burst
+    // x 1.05), so the unchanged roofline-lower-bound check stays a valid
+    // necessary condition on the real trace.
+    HardwareConfig hw = planned_on;
+    hw.name = "b200-measured";
+    const double head = 1.05;
+    hw.bw_gpu = std::max(r.h2d_bps, r.d2h_bps) * head;
+    hw.n_ssd = 1;
+    hw.bw_s2c = r.file_read_bps > 0 ? r.file_read_bps * head : 1e15;
+    hw.bw_c2s = r.file_write_bps > 0 ? r.file_write_bps * head : 1e15;
+    hw.cpu_opt_tput = r.optimizer_params_per_s * head;
+    hw.gpu_tput = r.compute_flops;
+    if (r.gpu_mem) hw.gpu_mem = r.gpu_mem;
+    if (r.cpu_mem) hw.cpu_mem = r.cpu_mem;
+    return hw;
+}
+
+} // namespace offsim

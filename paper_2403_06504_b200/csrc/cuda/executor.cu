@@ -1,0 +1,713 @@
+// B200 graph executor: runs every task of the tier-mapped graph on real
+// engines and returns the real SimTrace (include/offsim/exec.hpp).
+//
+// Lanes -> engines (one CUDA stream each, so every lane is serial, as the
+// reference's lane model and check_trace_invariants require):
+//   gpu_compute  synthetic fwd/bwd compute (timed kernel, work / rate)
+//   cpu_compute  the optimizer lane: fused AdamW kernel (fy::launch_adamw)
+//   link_c2g     H2D copy engine      link_g2c   D2H copy engine
+//   link_ssd     file tier: pread/pwrite (O_DIRECT) in stream host callbacks
+//                host tier: no bytes (zero-length tasks)
+// Each task is bracketed by two CUDA events on its lane stream; a task waits
+// on the end events of its dependencies on other lanes. Tasks are issued in
+// the start order of simulate(mapped graph, measured B200 rates), so each
+// engine executes the planned order and every awaited event has already been
+// recorded when the wait is enqueued.
+
+#include "adamw_kernels.cuh"
+#include "pipeline.cuh"
+
+#include "offsim/errors.hpp"
+#include "offsim/exec.hpp"
+
+#include <cuda_runtime.h>
+
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <sstream>
+
+namespace offsim {
+
+namespace {
+
+using fy::check_cuda;
+
+constexpr std::uint64_t kAlign = 4096;
+std::uint64_t round_up(std::uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// ------------------------------------------------------------ kernels
+
+__global__ void spin_kernel(std::uint64_t ns) {
+    std::uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
+__device__ __forceinline__ std::uint64_t mix64(std::uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// Deterministic byte pattern for activation / checkpoint buffers.
+__global__ void fill_pattern(std::uint64_t* p, std::uint64_t words, std::uint64_t seed) {
+    for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < words;
+         i += std::uint64_t(gridDim.x) * blockDim.x)
+        p[i] = mix64(seed ^ (i * 0x100000001b3ull));
+}
+
+// Synthetic optimizer state: master ~ U(-0.02,0.02)-ish, m small, v >= 0,
+// bf16 grads ~ 1e-3 (shape of SURVEY.md §8d; exact distribution irrelevant).
+__global__ void fill_states(float* st, std::uint64_t n, std::uint64_t seed) {
+    for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += std::uint64_t(gridDim.x) * blockDim.x) {
+        const std::uint64_t r = mix64(seed ^ i);
+        const float u0 = float(r & 0xffffff) / 16777216.0f - 0.5f;
+        const float u1 = float((r >> 24) & 0xffffff) / 16777216.0f - 0.5f;
+        st[i] = 0.04f * u0;
+        st[n + i] = 2e-3f * u1;
+        st[2 * n + i] = 1e-6f * (u0 * u0 + 1e-3f);
+    }
+}
+
+__global__ void fill_grads(std::uint16_t* g, std::uint64_t n, std::uint64_t seed) {
+    for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += std::uint64_t(gridDim.x) * blockDim.x) {
+        const float u = float(mix64(seed ^ (i + 0x51ed27)) & 0xffffff) / 16777216.0f - 0.5f;
+        const float f = 2e-3f * u;
+        g[i] = static_cast<std::uint16_t>(__float_as_uint(f) >> 16);
+    }
+}
+
+__global__ void count_mismatch(const std::uint64_t* a, const std::uint64_t* b, std::uint64_t words,
+                               unsigned long long* bad) {
+    unsigned long long local = 0;
+    for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < words;
+         i += std::uint64_t(gridDim.x) * blockDim.x)
+        local += a[i] != b[i];
+    if (local) atomicAdd(bad, local);
+}
+
+// --------------------------------------------------------- file tier
+
+struct IoRequest {
+    int fd = -1;
+    void* buf = nullptr;
+    std::uint64_t bytes = 0; // rounded to kAlign for O_DIRECT
+    std::uint64_t offset = 0;
+    bool write = false;
+    bool poison_after = false; // overwrite the host buffer after a write
+    std::atomic<int>* error = nullptr;
+    std::string* error_text = nullptr;
+    std::mutex* error_mu = nullptr;
+};
+
+void CUDART_CB run_io(void* arg) {
+    auto* r = static_cast<IoRequest*>(arg);
+    std::uint64_t done = 0;
+    while (done < r->bytes) {
+        char* p = static_cast<char*>(r->buf) + done;
+        const std::uint64_t left = r->bytes - done;
+        const ssize_t n = r->write ? ::pwrite(r->fd, p, left, static_cast<off_t>(r->offset + done))
+                                   : ::pread(r->fd, p, left, static_cast<off_t>(r->offset + done));
+        if (n < 0 && errno == EINTR) continue;
+        if (n <= 0) {
+            std::lock_guard<std::mutex> lk(*r->error_mu);
+            r->error->store(1);
+            *r->error_text = std::string(r->write ? "pwrite" : "pread") + " failed: " +
+                             (n < 0 ? std::strerror(errno) : "short read");
+            return;
+        }
+        done += static_cast<std::uint64_t>(n);
+    }
+    if (r->write && r->poison_after) std::memset(r->buf, 0xA5, r->bytes);
+}
+
+class TierFile {
+public:
+    TierFile(const std::string& path, std::uint64_t size, bool direct) : path_(path) {
+        int flags = O_RDWR | O_CREAT | O_TRUNC;
+        if (direct) flags |= O_DIRECT;
+        fd_ = ::open(path.c_str(), flags, 0600);
+        if (fd_ < 0 && direct) fd_ = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
+        if (fd_ < 0) throw InfeasibleError("cannot open tier file " + path + ": " + std::strerror(errno));
+        if (::ftruncate(fd_, static_cast<off_t>(size)) != 0)
+            throw InfeasibleError("cannot size tier file " + path + ": " + std::strerror(errno));
+    }
+    ~TierFile() {
+        if (fd_ >= 0) ::close(fd_);
+        ::unlink(path_.c_str());
+    }
+    int fd() const { return fd_; }
+
+private:
+    std::string path_;
+    int fd_ = -1;
+};
+
+// ------------------------------------------------------------- parsing
+
+enum class Op { noop, h2d, d2h, file_read, file_write, compute, update };
+
+struct Parsed {
+    std::string phase, what; // "fwd","p_c2g"
+    std::uint32_t block = 0;
+    int layer = -1; // 0..3 within the block when present
+};
+
+Parsed parse_name(const std::string& name) {
+    // "<phase> <what> <b|g><k>[ <layer kind>]"
+    Parsed p;
+    std::istringstream is(name);
+    std::string tag, kind;
+    is >> p.phase >> p.what >> tag >> kind;
+    p.block = static_cast<std::uint32_t>(std::stoul(tag.substr(1)));
+    static const char* kKinds[] = {"linear_qkv", "linear_htoh", "linear_hto4h", "linear_4htoh"};
+    for (int j = 0; j < 4; ++j)
+        if (kind == kKinds[j]) p.layer = j;
+    return p;
+}
+
+struct Pinned {
+    void* p = nullptr;
+    Pinned() = default;
+    explicit Pinned(std::uint64_t bytes) {
+        check_cuda(cudaHostAlloc(&p, std::max<std::uint64_t>(bytes, kAlign), cudaHostAllocPortable),
+                   "cudaHostAlloc (executor host buffers)");
+    }
+    Pinned(Pinned&& o) noexcept : p(o.p) { o.p = nullptr; }
+    Pinned& operator=(Pinned&& o) noexcept {
+        std::swap(p, o.p);
+        return *this;
+    }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+struct Device {
+    void* p = nullptr;
+    Device() = default;
+    explicit Device(std::uint64_t bytes) {
+        const cudaError_t e = cudaMalloc(&p, std::max<std::uint64_t>(bytes, 256));
+        if (e == cudaErrorMemoryAllocation)
+            throw InfeasibleError("device allocation of " + std::to_string(bytes) + " bytes failed");
+        check_cuda(e, "cudaMalloc (executor)");
+    }
+    Device(Device&& o) noexcept : p(o.p) { o.p = nullptr; }
+    Device& operator=(Device&& o) noexcept {
+        std::swap(p, o.p);
+        return *this;
+    }
+    ~Device() {
+        if (p) cudaFree(p);
+    }
+};
+
+// --------------------------------------------------------------- engine
+
+class Engine {
+public:
+    Engine(const ModelConfig& model, const SwapPlan& plan, const TaskGraph& mapped,
+           const ExecOptions& opt, const std::vector<ChunkBuffers>* chunks)
+        : model_(model), plan_(plan), g_(mapped), opt_(opt), user_(chunks) {}
+
+    ~Engine() {
+        for (cudaEvent_t e : events_) cudaEventDestroy(e);
+        if (base_) cudaEventDestroy(base_);
+        for (cudaStream_t s : streams_)
+            if (s) cudaStreamDestroy(s);
+    }
+
+    void setup();
+    MeasuredRates calibrate();
+    void run(const SimTrace& planned, ExecReport& rep);
+
+private:
+    cudaStream_t lane_stream(ResourceId r) const { return streams_[static_cast<int>(r)]; }
+    void issue(const Task& t, ExecReport& rep);
+    std::uint64_t layer_offset(int j) const; // byte offset of layer j inside the block params
+
+    const ModelConfig& model_;
+    const SwapPlan& plan_;
+    const TaskGraph& g_;
+    ExecOptions opt_;
+    const std::vector<ChunkBuffers>* user_;
+
+    std::uint32_t blocks_ = 0;
+    std::uint64_t n_ = 0;          // params per block (chunk)
+    std::vector<LayerProfile> layers_;
+    std::vector<bool> swapped_;
+    std::uint64_t ckpt_bytes_ = 0;
+    bool file_tier_ = false;
+
+    cudaStream_t streams_[5] = {};
+    std::vector<cudaEvent_t> events_;
+    cudaEvent_t base_ = nullptr;
+
+    // host side
+    std::vector<Pinned> own_states_, own_params_, act_host_, ckpt_host_, grad_host_;
+    std::vector<void*> h_states_, h_params_;
+    // device side
+    std::vector<Device> own_grads_, act_dev_, act_restore_, ckpt_dev_, ckpt_restore_, slots_;
+    std::vector<const void*> d_grads_;
+    Device wscratch_[2];
+    int wscratch_turn_ = 0;
+    Device workspace_, d_norm_, d_bad_, d_mismatch_;
+    int slot_of(std::uint32_t block) const {
+        // optimizer groups run in reverse block order: m = blocks - 1 - k
+        return static_cast<int>((blocks_ - 1 - block) % slots_.size());
+    }
+
+    // file tier
+    std::unique_ptr<TierFile> f_states_, f_params_, f_acts_, f_grads_;
+    std::vector<std::uint64_t> act_file_off_;
+    std::vector<std::uint64_t> ckpt_file_off_;
+    std::vector<std::unique_ptr<IoRequest>> io_;
+    std::atomic<int> io_error_{0};
+    std::string io_error_text_;
+    std::mutex io_mu_;
+
+    fy::AdamScalars scalars_{};
+    double compute_rate_ = 0.0;
+};
+
+std::uint64_t Engine::layer_offset(int j) const {
+    std::uint64_t off = 0;
+    for (int k = 0; k < j; ++k) off += layers_[k].param_bytes;
+    return off;
+}
+
+void Engine::setup() {
+    check_cuda(cudaSetDevice(opt_.device), "cudaSetDevice");
+    blocks_ = model_.num_layers;
+    n_ = 12ull * model_.hidden_dim * model_.hidden_dim;
+    layers_ = build_layer_profiles(model_);
+    swapped_.assign(layers_.size(), false);
+    for (std::uint32_t i : plan_.swapped_layers) swapped_[i] = true;
+    ckpt_bytes_ = footprint(model_).checkpoint_bytes_per_block;
+    file_tier_ = opt_.tier == StateTier::file;
+    if (model_.param_elem_bytes != 2)
+        throw ConfigError("executor: param_elem_bytes must be 2 (bf16 params)");
+    if (std::llround(model_.optimizer_state_multiplier) != 6)
+        throw ConfigError("executor: optimizer_state_multiplier must be 6 (fp32 master, m, v)");
+    if (user_ && user_->size() != blocks_)
+        throw ConfigError("executor: expected one ChunkBuffers per block");
+
+    int lo = 0, hi = 0;
+    check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
+    for (int r = 0; r < 5; ++r) {
+        const int prio = r == static_cast<int>(ResourceId::cpu_compute) ? hi : lo;
+        check_cuda(cudaStreamCreateWithPriority(&streams_[r], cudaStreamNonBlocking, prio), "stream");
+    }
+    events_.resize(2 * g_.tasks.size());
+    for (cudaEvent_t& e : events_) check_cuda(cudaEventCreate(&e), "event");
+    check_cuda(cudaEventCreate(&base_), "event");
+
+    const std::uint64_t state_b = 12 * n_, param_b = 2 * n_;
+    const std::uint64_t seed = opt_.seed * 0x9e3779b97f4a7c15ull + 17;
+    // optimizer states + params (host), grads (device)
+    h_states_.resize(blocks_);
+    h_params_.resize(blocks_);
+    d_grads_.resize(blocks_);
+    for (std::uint32_t k = 0; k < blocks_; ++k) {
+        if (user_ && (*user_)[k].host_states) {
+            h_states_[k] = (*user_)[k].host_states;
+            h_params_[k] = (*user_)[k].host_params;
+        } else {
+            own_states_.emplace_back(round_up(state_b));
+            own_params_.emplace_back(round_up(param_b));
+            h_states_[k] = own_states_.back().p;
+            h_params_[k] = own_params_.back().p;
+        }
+        if (user_ && (*user_)[k].device_grads) {
+            d_grads_[k] = (*user_)[k].device_grads;
+        } else {
+            own_grads_.emplace_back(param_b);
+            d_grads_[k] = own_grads_.back().p;
+            fill_grads<<<592, 256>>>(static_cast<std::uint16_t*>(own_grads_.back().p), n_, seed + 31 * k);
+        }
+    }
+    // synthetic host states when not provided: generate on the device, copy
+    if (!(user_ && (*user_)[0].host_states)) {
+        Device tmp(state_b);
+        for (std::uint32_t k = 0; k < blocks_; ++k) {
+            fill_states<<<592, 256>>>(static_cast<float*>(tmp.p), n_, seed + 7 * k);
+            check_cuda(cudaMemcpy(h_states_[k], tmp.p, state_b, cudaMemcpyDeviceToHost), "seed states");
+            std::memset(h_params_[k], 0, param_b);
+        }
+    }
+    const std::uint32_t slots = std::max<std::uint32_t>(2, opt_.state_slots);
+    for (std::uint32_t s = 0; s < slots; ++s) slots_.emplace_back(state_b);
+
+    std::uint64_t max_w = 0;
+    for (const LayerProfile& l : layers_) max_w = std::max(max_w, l.param_bytes);
+    wscratch_[0] = Device(max_w);
+    wscratch_[1] = Device(max_w);
+
+    // activation / checkpoint units: device originals (pattern), device
+    // restore targets, pinned host landing buffers
+    act_dev_.resize(layers_.size());
+    act_restore_.resize(layers_.size());
+    act_host_.resize(layers_.size());
+    for (std::size_t i = 0; i < layers_.size(); ++i) {
+        if (!swapped_[i]) continue;
+        const std::uint64_t b = round_up(layers_[i].act_bytes);
+        act_dev_[i] = Device(b);
+        act_restore_[i] = Device(b);
+        act_host_[i] = Pinned(b);
+        fill_pattern<<<296, 256>>>(static_cast<std::uint64_t*>(act_dev_[i].p), b / 8, seed ^ (i + 1));
+    }
+    for (std::uint32_t k = 0; k < blocks_; ++k) {
+        const std::uint64_t b = round_up(ckpt_bytes_);
+        ckpt_dev_.emplace_back(b);
+        ckpt_restore_.emplace_back(b);
+        ckpt_host_.emplace_back(b);
+        fill_pattern<<<296, 256>>>(static_cast<std::uint64_t*>(ckpt_dev_.back().p), b / 8,
+                                   seed ^ (0xc0ffee00ull + k));
+    }
+    if (g_.header.variant != ScheduleVariant::overlapped)
+        for (std::uint32_t k = 0; k < blocks_; ++k) grad_host_.emplace_back(round_up(param_b));
+
+    workspace_ = Device(sizeof(float) * fy::kWorkspaceFloats);
+    d_norm_ = Device(sizeof(double));
+    d_bad_ = Device(sizeof(int));
+    d_mismatch_ = Device(sizeof(unsigned long long));
+    check_cuda(cudaMemset(d_norm_.p, 0, sizeof(double)), "memset");
+    check_cuda(cudaMemset(d_bad_.p, 0, sizeof(int)), "memset");
+    check_cuda(cudaMemset(d_mismatch_.p, 0, sizeof(unsigned long long)), "memset");
+
+    if (file_tier_) {
+        ::mkdir(opt_.file_dir.c_str(), 0700);
+        const bool direct = opt_.direct_io && model_.hidden_dim % 64 == 0;
+        const std::string stem = opt_.file_dir + "/offsim_" + std::to_string(::getpid()) + "_";
+        f_states_ = std::make_unique<TierFile>(stem + "states.bin", blocks_ * round_up(state_b), direct);
+        f_params_ = std::make_unique<TierFile>(stem + "params.bin", blocks_ * round_up(param_b), direct);
+        std::uint64_t off = 0;
+        act_file_off_.assign(layers_.size(), 0);
+        for (std::size_t i = 0; i < layers_.size(); ++i)
+            if (swapped_[i]) {
+                act_file_off_[i] = off;
+                off += round_up(layers_[i].act_bytes);
+            }
+        for (std::uint32_t k = 0; k < blocks_; ++k) {
+            ckpt_file_off_.push_back(off);
+            off += round_up(ckpt_bytes_);
+        }
+        f_acts_ = std::make_unique<TierFile>(stem + "acts.bin", std::max<std::uint64_t>(off, kAlign), direct);
+        if (!grad_host_.empty())
+            f_grads_ = std::make_unique<TierFile>(stem + "grads.bin", blocks_ * round_up(param_b), direct);
+        // the tier holds the initial states / params before the step
+        for (std::uint32_t k = 0; k < blocks_; ++k) {
+            IoRequest w{f_states_->fd(), h_states_[k], round_up(state_b), k * round_up(state_b), true,
+                        false, &io_error_, &io_error_text_, &io_mu_};
+            run_io(&w);
+            IoRequest wp{f_params_->fd(), h_params_[k], round_up(param_b), k * round_up(param_b), true,
+                         false, &io_error_, &io_error_text_, &io_mu_};
+            run_io(&wp);
+        }
+        if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
+    }
+    const AdamHyper& a = opt_.adam;
+    scalars_ = fy::make_scalars(a.lr, a.beta1, a.beta2, a.eps, a.weight_decay, a.step,
+                                a.adamw_mode, a.bias_correction, a.grad_scale);
+    check_cuda(cudaDeviceSynchronize(), "executor setup");
+}
+
+MeasuredRates Engine::calibrate() {
+    // Burst rates of the engines this run will use (upper bounds for the
+    // DES order and the roofline check).
+    MeasuredRates r;
+    const std::uint64_t bytes = std::min<std::uint64_t>(12 * n_, 512ull << 20);
+    Pinned h(bytes);
+    cudaEvent_t a, b;
+    check_cuda(cudaEventCreate(&a), "event");
+    check_cuda(cudaEventCreate(&b), "event");
+    auto timed = [&](cudaStream_t s, auto&& fn) {
+        float best = 1e30f;
+        for (int it = 0; it < 3; ++it) {
+            check_cuda(cudaEventRecord(a, s), "record");
+            fn(s);
+            check_cuda(cudaEventRecord(b, s), "record");
+            check_cuda(cudaEventSynchronize(b), "sync");
+            float ms = 0;
+            check_cuda(cudaEventElapsedTime(&ms, a, b), "elapsed");
+            best = std::min(best, ms);
+        }
+        return best * 1e-3;
+    };
+    void* slot = slots_[0].p;
+    r.h2d_bps = bytes / timed(lane_stream(ResourceId::link_c2g), [&](cudaStream_t s) {
+                    check_cuda(cudaMemcpyAsync(slot, h.p, bytes, cudaMemcpyHostToDevice, s), "h2d");
+                });
+    r.d2h_bps = bytes / timed(lane_stream(ResourceId::link_g2c), [&](cudaStream_t s) {
+                    check_cuda(cudaMemcpyAsync(h.p, slot, bytes, cudaMemcpyDeviceToHost, s), "d2h");
+                });
+    // fused kernel rate on a scratch copy (does not touch the real states)
+    {
+        Device st(12 * n_), gr(2 * n_);
+        fill_states<<<592, 256>>>(static_cast<float*>(st.p), n_, 1);
+        fill_grads<<<592, 256>>>(static_cast<std::uint16_t*>(gr.p), n_, 2);
+        fy::AdamLaunch l{};
+        l.master = static_cast<float*>(st.p);
+        l.m = l.master + n_;
+        l.v = l.master + 2 * n_;
+        l.grad = gr.p;
+        l.grad_dtype = 0;
+        l.param = gr.p;
+        l.param_dtype = 0;
+        l.n = n_;
+        l.s = scalars_;
+        const double sec = timed(lane_stream(ResourceId::cpu_compute), [&](cudaStream_t s) {
+            check_cuda(fy::launch_adamw(l, s), "calibrate adamw");
+        });
+        r.optimizer_params_per_s = n_ / sec;
+    }
+    if (file_tier_) {
+        IoRequest w{f_states_->fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
+                    &io_error_text_, &io_mu_};
+        const auto t0 = std::chrono::steady_clock::now();
+        run_io(&w);
+        ::fdatasync(f_states_->fd());
+        const auto t1 = std::chrono::steady_clock::now();
+        IoRequest rd = w;
+        rd.write = false;
+        run_io(&rd);
+        const auto t2 = std::chrono::steady_clock::now();
+        r.file_write_bps = bytes / std::chrono::duration<double>(t1 - t0).count();
+        r.file_read_bps = bytes / std::chrono::duration<double>(t2 - t1).count();
+        // restore the block-0 states the calibration write clobbered
+        IoRequest fix{f_states_->fd(), h_states_[0], round_up(12 * n_), 0, true, false, &io_error_,
+                      &io_error_text_, &io_mu_};
+        run_io(&fix);
+        if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
+    }
+    r.compute_flops = opt_.compute_rate > 0 ? opt_.compute_rate : 0.0;
+    std::size_t free_b = 0, total_b = 0;
+    check_cuda(cudaMemGetInfo(&free_b, &total_b), "meminfo");
+    r.gpu_mem = total_b;
+    r.cpu_mem = static_cast<std::uint64_t>(::sysconf(_SC_PHYS_PAGES)) *
+                static_cast<std::uint64_t>(::sysconf(_SC_PAGESIZE));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return r;
+}
+
+void Engine::issue(const Task& t, ExecReport& rep) {
+    cudaStream_t s = lane_stream(t.resource);
+    for (const std::uint32_t d : t.deps)
+        if (g_.tasks[d].resource != t.resource)
+            check_cuda(cudaStreamWaitEvent(s, events_[2 * d + 1], 0), "wait dep");
+    const Parsed p = parse_name(t.name);
+    const std::uint32_t k = p.block;
+    const int j = p.layer;
+    const std::uint64_t li = j >= 0 ? 4ull * k + j : 0;
+    auto phys = [&](const char* engine, std::uint64_t bytes) {
+        rep.physical_bytes[std::string(engine) + "/" + to_string(t.payload)] += static_cast<double>(bytes);
+    };
+    auto h2d = [&](void* dst, const void* src, std::uint64_t bytes) {
+        check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+        phys("h2d", bytes);
+    };
+    auto d2h = [&](void* dst, const void* src, std::uint64_t bytes) {
+        check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+        phys("d2h", bytes);
+    };
+    auto file = [&](const TierFile& f, void* buf, std::uint64_t bytes, std::uint64_t off, bool write,
+                    bool poison) {
+        io_.push_back(std::make_unique<IoRequest>(IoRequest{f.fd(), buf, round_up(bytes), off, write,
+                                                            poison, &io_error_, &io_error_text_, &io_mu_}));
+        check_cuda(cudaLaunchHostFunc(s, run_io, io_.back().get()), "host io");
+        phys(write ? "file_write" : "file_read", bytes);
+    };
+
+    check_cuda(cudaEventRecord(events_[2 * t.id], s), "record");
+    const std::uint64_t state_b = 12 * n_, param_b = 2 * n_;
+    const std::string& w = p.what;
+    if (t.work <= 0.0) {
+        // zero-byte task of the mapped graph (host tier SSD hop, HBM grads)
+    } else if (t.kind == TaskKind::compute) {
+        const double sec = t.work / compute_rate_;
+        spin_kernel<<<1, 32, 0, s>>>(static_cast<std::uint64_t>(sec * 1e9));
+        check_cuda(cudaGetLastError(), "compute launch");
+        ++rep.kernel_launches;
+    } else if (t.kind == TaskKind::optimizer_update) {
+        const int slot = slot_of(k);
+        fy::AdamLaunch l{};
+        l.master = static_cast<float*>(slots_[slot].p);
+        l.m = l.master + n_;
+        l.v = l.master + 2 * n_;
+        l.grad = d_grads_[k];
+        l.grad_dtype = 0;
+        l.param = const_cast<void*>(d_grads_[k]); // grad buffer becomes the params
+        l.param_dtype = 0;
+        l.n = n_;
+        l.s = scalars_;
+        l.grad_sq_sum = static_cast<double*>(d_norm_.p);
+        l.accumulate_sq = 1;
+        l.workspace = static_cast<float*>(workspace_.p);
+        l.nonfinite = static_cast<int*>(d_bad_.p);
+        check_cuda(fy::launch_adamw(l, s), "opt update");
+        rep.kernel_launches += 2;
+    } else if (w == "state_h2d") {
+        // the slot's previous user (state_d2h of group m - slots) is a dep
+        h2d(slots_[slot_of(k)].p, h_states_[k], state_b);
+    } else if (w == "state_d2h") {
+        d2h(h_states_[k], slots_[slot_of(k)].p, state_b);
+    } else if (w == "param_d2h") {
+        d2h(h_params_[k], d_grads_[k], param_b);
+    } else if (w == "state_s2c") {
+        file(*f_states_, h_states_[k], state_b, k * round_up(state_b), false, false);
+    } else if (w == "state_c2s") {
+        file(*f_states_, h_states_[k], state_b, k * round_up(state_b), true, false);
+    } else if (w == "param_c2s") {
+        file(*f_params_, h_params_[k], param_b, k * round_up(param_b), true, false);
+    } else if (w == "p_s2c") {
+        const std::uint64_t off = layer_offset(j);
+        file(*f_params_, static_cast<char*>(h_params_[k]) + off, layers_[li].param_bytes,
+             k * round_up(param_b) + off, false, false);
+    } else if (w == "p_c2g") {
+        void* dst = wscratch_[wscratch_turn_ ^= 1].p;
+        h2d(dst, static_cast<char*>(h_params_[k]) + layer_offset(j), layers_[li].param_bytes);
+    } else if (w == "act_g2c") {
+        d2h(act_host_[li].p, act_dev_[li].p, layers_[li].act_bytes);
+    } else if (w == "act_c2s") {
+        file(*f_acts_, act_host_[li].p, layers_[li].act_bytes, act_file_off_[li], true, opt_.verify_swaps);
+    } else if (w == "act_s2c") {
+        file(*f_acts_, act_host_[li].p, layers_[li].act_bytes, act_file_off_[li], false, false);
+    } else if (w == "act_c2g") {
+        h2d(act_restore_[li].p, act_host_[li].p, layers_[li].act_bytes);
+    } else if (w == "ckpt_g2c") {
+        d2h(ckpt_host_[k].p, ckpt_dev_[k].p, ckpt_bytes_);
+    } else if (w == "ckpt_c2s") {
+        file(*f_acts_, ckpt_host_[k].p, ckpt_bytes_, ckpt_file_off_[k], true, opt_.verify_swaps);
+    } else if (w == "ckpt_s2c") {
+        file(*f_acts_, ckpt_host_[k].p, ckpt_bytes_, ckpt_file_off_[k], false, false);
+    } else if (w == "ckpt_c2g") {
+        h2d(ckpt_restore_[k].p, ckpt_host_[k].p, ckpt_bytes_);
+    } else if (w == "grad_g2c") {
+        d2h(grad_host_[k].p, d_grads_[k], param_b);
+    } else if (w == "grad_c2s") {
+        file(*f_grads_, grad_host_[k].p, param_b, k * round_up(param_b), true, false);
+    } else if (w == "grad_s2c") {
+        file(*f_grads_, grad_host_[k].p, param_b, k * round_up(param_b), false, false);
+    } else if (w == "grad_h2d") {
+        h2d(const_cast<void*>(d_grads_[k]), grad_host_[k].p, param_b);
+    } else {
+        throw InvariantError("executor: no operation for task '" + t.name + "'");
+    }
+    check_cuda(cudaEventRecord(events_[2 * t.id + 1], s), "record");
+}
+
+void Engine::run(const SimTrace& planned, ExecReport& rep) {
+    compute_rate_ = rep.hw_exec.gpu_tput;
+    // issue order = planned start order (ties: task id, always topological)
+    std::vector<std::pair<std::uint64_t, std::uint32_t>> order;
+    order.reserve(planned.events.size());
+    for (const TraceEvent& e : planned.events) order.emplace_back(e.start_ns, e.task_id);
+    std::sort(order.begin(), order.end());
+
+    check_cuda(cudaDeviceSynchronize(), "pre-run sync");
+    check_cuda(cudaEventRecord(base_, streams_[0]), "base");
+    for (int r = 1; r < 5; ++r) check_cuda(cudaStreamWaitEvent(streams_[r], base_, 0), "base wait");
+    const auto wall0 = std::chrono::steady_clock::now();
+    for (const auto& [start, id] : order) issue(g_.tasks[id], rep);
+    check_cuda(cudaDeviceSynchronize(), "executor run");
+    (void)wall0;
+    if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
+
+    // swap integrity: every restored buffer equals its original
+    if (opt_.verify_swaps) {
+        auto cmp = [&](const Device& a, const Device& b, std::uint64_t bytes) {
+            count_mismatch<<<296, 256>>>(static_cast<const std::uint64_t*>(a.p),
+                                        static_cast<const std::uint64_t*>(b.p), bytes / 8,
+                                        static_cast<unsigned long long*>(d_mismatch_.p));
+            ++rep.swap_checks;
+        };
+        for (const Task& t : g_.tasks) {
+            if (t.work <= 0.0) continue;
+            const Parsed p = parse_name(t.name);
+            if (p.what == "act_c2g") cmp(act_dev_[4ull * p.block + p.layer], act_restore_[4ull * p.block + p.layer],
+                                         layers_[4ull * p.block + p.layer].act_bytes / 8 * 8);
+            if (p.what == "ckpt_c2g") cmp(ckpt_dev_[p.block], ckpt_restore_[p.block], ckpt_bytes_ / 8 * 8);
+        }
+        unsigned long long bad = 0;
+        check_cuda(cudaMemcpy(&bad, d_mismatch_.p, sizeof bad, cudaMemcpyDeviceToHost), "mismatch");
+        rep.swap_mismatches = bad;
+    }
+    check_cuda(cudaMemcpy(&rep.grad_sq_sum, d_norm_.p, sizeof(double), cudaMemcpyDeviceToHost), "norm");
+    check_cuda(cudaMemcpy(&rep.nonfinite, d_bad_.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+
+    // real trace from the events
+    SimTrace& tr = rep.trace;
+    tr.header = g_.header;
+    tr.events.clear();
+    for (const Task& t : g_.tasks) {
+        float ms0 = 0, ms1 = 0;
+        check_cuda(cudaEventElapsedTime(&ms0, base_, events_[2 * t.id]), "elapsed");
+        check_cuda(cudaEventElapsedTime(&ms1, base_, events_[2 * t.id + 1]), "elapsed");
+        TraceEvent e{t.id, t.resource, t.dir, t.payload, t.work,
+                     static_cast<std::uint64_t>(std::llround(std::max(0.0f, ms0) * 1e6)),
+                     static_cast<std::uint64_t>(std::llround(std::max(0.0f, ms1) * 1e6))};
+        if (e.end_ns < e.start_ns) e.end_ns = e.start_ns;
+        tr.events.push_back(e);
+        tr.makespan_ns = std::max(tr.makespan_ns, e.end_ns);
+        tr.busy_ns[t.resource] += e.end_ns - e.start_ns;
+    }
+    std::sort(tr.events.begin(), tr.events.end(), [](const TraceEvent& a, const TraceEvent& b) {
+        return a.end_ns != b.end_ns ? a.end_ns < b.end_ns : a.task_id < b.task_id;
+    });
+    // peak memory by replaying the effects over the real timeline
+    std::vector<std::tuple<std::uint64_t, int, std::uint32_t>> edges;
+    for (const TraceEvent& e : tr.events) {
+        edges.emplace_back(e.start_ns, 1, e.task_id);
+        edges.emplace_back(e.end_ns, 0, e.task_id);
+    }
+    std::sort(edges.begin(), edges.end());
+    std::map<ResourceId, std::int64_t> level = g_.initial_mem;
+    tr.peak_mem = level;
+    for (const auto& [time, is_start, id] : edges) {
+        for (const MemEffect& fx : g_.tasks[id].mem_effects) {
+            if (fx.at_start != (is_start == 1)) continue;
+            level[fx.mem] += fx.delta_bytes;
+            tr.peak_mem[fx.mem] = std::max(tr.peak_mem[fx.mem], level[fx.mem]);
+        }
+    }
+}
+
+} // namespace
+
+ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const SwapPlan& plan,
+                   ScheduleVariant variant, const ExecOptions& options,
+                   const std::vector<ChunkBuffers>* chunks) {
+    ExecReport rep;
+    const TaskGraph reference = build_schedule(model, hw, plan, variant);
+    for (const Task& t : reference.tasks)
+        if (t.kind == TaskKind::transfer)
+            rep.reference_bytes[std::string(to_string(t.resource)) + "/" + to_string(t.payload)] += t.work;
+    rep.graph = map_graph_for_b200(reference, options.tier, std::max<std::uint32_t>(2, options.state_slots));
+
+    Engine eng(model, plan, rep.graph, options, chunks);
+    eng.setup();
+    MeasuredRates rates = eng.calibrate();
+    if (rates.compute_flops <= 0) rates.compute_flops = hw.gpu_tput;
+    rep.hw_exec = b200_hardware(hw, rates);
+    rep.planned = simulate(rep.graph, rep.hw_exec);
+    eng.run(rep.planned, rep);
+    rep.invariants = check_trace_invariants(rep.graph, rep.trace, rep.hw_exec);
+    return rep;
+}
+
+} // namespace offsim

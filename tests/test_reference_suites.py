@@ -1,0 +1,48 @@
+"""CPU: the reference's OWN test suites, unmodified, run against this repo's
+implementation (drop-in check of the C++ API and the C ABI):
+  build/ref_unit_tests_on_b200   proj/tests/test_{workload,hardware,cost_model,
+                                 planner,sim,capacity,scenario}.cpp + main.cpp
+                                 on the doctest shim, linked to this core
+  build/ref_capi_tests_on_b200   proj/tests/test_capi.cpp linked to
+                                 paper_2403_06504_b200/lib/liboffsim.so.0
+  build/ref_acceptance_on_b200   proj/tests/acceptance/acceptance_main.cpp
+They are compiled by `make reftests` where /root/reference exists; the shim
+is calibrated by the same suites passing against the compiled reference
+(oracle/_ref/ref_unit_tests, ref_capi_tests)."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+SUITES = ["workload", "hardware", "cost_model", "planner", "sim", "capacity", "scenario"]
+
+
+def _run(exe, *args):
+    if not exe.exists():
+        pytest.skip(f"{exe.name} not built (needs /root/reference at build time)")
+    return subprocess.run([str(exe), *args], capture_output=True, text=True, timeout=600)
+
+
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_unit_suite_on_b200_core(suite):
+    r = _run(ROOT / "build" / "ref_unit_tests_on_b200", f"--test-suite={suite}")
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "0 failed" in r.stdout and "test cases: 0 " not in r.stdout
+
+
+def test_reference_capi_suite_on_product_library():
+    r = _run(ROOT / "build" / "ref_capi_tests_on_b200")
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "6 passed" in r.stdout
+
+
+def test_reference_acceptance_on_b200_core():
+    r = _run(ROOT / "build" / "ref_acceptance_on_b200")
+    assert r.returncode == 0, r.stdout[-2000:]
+    assert "ACCEPTANCE: 9/9 criteria passed" in r.stdout
+
+
+def test_shim_calibrated_against_reference():
+    r = _run(ROOT / "oracle" / "_ref" / "ref_unit_tests")
+    assert r.returncode == 0 and "54 passed" in r.stdout

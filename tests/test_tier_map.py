@@ -1,0 +1,64 @@
+"""CPU: the B200 tier map (map_graph_for_b200) through offsim_execute's dry
+run — inserted optimizer hops, bytes that stay in HBM / pinned DRAM, the
+slot-reuse edges, and the UNCHANGED trace invariants on the mapped graph."""
+import pytest
+
+from exec_api import execute, scenario
+
+C1 = scenario()                                       # GPT-2-small shape, b=8
+C1_SSD = scenario(hardware='{"preset": "a100-12ssd", "cpu_mem": 1000000000}')
+C2 = scenario(40, 40, 5120, 32, 1024, name="gpt3-13b")
+N1, L1 = 12 * 768 * 768, 12
+N2, L2 = 12 * 5120 * 5120, 40
+
+
+@pytest.mark.parametrize("sc,N,L", [(C1, N1, L1), (C2, N2, L2)])
+def test_host_tier_overlapped(sc, N, L):
+    st, s, _, err = execute(sc, {"dry_run": True, "tier": "host"})
+    assert st == 0, err
+    assert s["all_invariants_pass"], s["invariants"]
+    assert s["task_count"] == s["reference_task_count"] + 3 * L
+    assert len(s["inserted_tasks"]) == 3 * L
+    mb = s["mapped_bytes"]
+    assert all(v == 0 for k, v in mb.items() if k.startswith("link_ssd/"))
+    assert mb.get("link_g2c/grads", 0) == 0          # grads stay in HBM
+    assert mb["link_c2g/opt_states"] == 12 * N * L     # states in (12 B/param)
+    assert mb["link_g2c/opt_states"] == 12 * N * L     # states out
+    ref = s["reference_bytes"]
+    assert mb["link_g2c/params"] == 2 * N * L          # bf16 params out
+    assert ref["link_ssd/opt_states"] == 24 * N * L    # reference: 12N read + 12N write
+
+
+def test_file_tier_keeps_reference_ssd_bytes():
+    st, s, _, err = execute(C1_SSD, {"dry_run": True, "tier": "file"})
+    assert st == 0, err
+    assert s["all_invariants_pass"], s["invariants"]
+    ref, mb = s["reference_bytes"], s["mapped_bytes"]
+    for k, v in ref.items():
+        if k.startswith("link_ssd/") and k != "link_ssd/grads":
+            assert mb[k] == v, k
+    assert any(k == "link_ssd/activations" for k in mb)  # checkpoints go to the file tier
+
+
+@pytest.mark.parametrize("variant", ["serial", "pipelined"])
+def test_non_overlapped_variants(variant):
+    sc = scenario(variant=variant)
+    st, s, _, err = execute(sc, {"dry_run": True, "tier": "host"})
+    assert st == 2 and "tier=file" in err
+    st, s, _, err = execute(sc, {"dry_run": True, "tier": "file"})
+    assert st == 0, err
+    names = {e["name"]: e["pass"] for e in s["invariants"]}
+    assert names["gradient-ssd-roundtrip"]
+    assert s["all_invariants_pass"], s["invariants"]
+    assert len(s["inserted_tasks"]) == 4 * L1  # + grad_h2d per group
+
+
+def test_slot_edges_and_bad_options():
+    st, s, _, err = execute(C1, {"dry_run": True, "state_slots": 2})
+    assert st == 0 and s["all_invariants_pass"]
+    st, _, _, err = execute(C1, {"dry_run": True, "state_slots": 1})
+    assert st == 2 and "state_slots" in err
+    st, _, _, err = execute(C1, {"dry_run": True, "colour": "red"})
+    assert st == 2 and "colour" in err
+    st, _, _, err = execute(C1, {"dry_run": True, "tier": "tape"})
+    assert st == 2
