@@ -108,6 +108,11 @@ fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad
                         double* grad_sq_sum, int accumulate_sq, float* workspace,
                         int* nonfinite_flag, void* stream);
 
+/* Tuning of the fused kernel (diagnostics / sweeps): quads (4 elements) per
+ * thread per grid-stride iteration in {1,2,4,8} (default 4) and resident CTAs
+ * per SM (0 = occupancy limit). Process-wide. */
+fy_status fy_adamw_tune(int unroll, int ctas_per_sm);
+
 /* Number of SMs and the launch geometry the kernels use on `device`
  * (diagnostics / roofline bookkeeping). */
 fy_status fy_device_info(int device, int* sm_count, int* ctas_per_sm, int* threads_per_cta);

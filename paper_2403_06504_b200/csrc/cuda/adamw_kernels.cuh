@@ -57,4 +57,8 @@ struct Geometry {
 };
 Geometry geometry(int device);
 
+// Tuning knobs of the vector kernel (quads per thread per iteration: 1, 2,
+// 4 or 8; resident CTAs per SM, 0 = occupancy limit). Diagnostics/sweeps.
+void set_tuning(int unroll, int ctas_per_sm);
+
 } // namespace fy

@@ -197,3 +197,11 @@ fy_status fy_host_free(void* p) {
 }
 
 } // extern "C"
+
+extern "C" fy_status fy_adamw_tune(int unroll, int ctas_per_sm) {
+    if (unroll != 1 && unroll != 2 && unroll != 4 && unroll != 8)
+        return fail(FY_ERR_CONFIG, "unroll must be 1, 2, 4 or 8");
+    if (ctas_per_sm < 0 || ctas_per_sm > 32) return fail(FY_ERR_CONFIG, "ctas_per_sm out of range");
+    fy::set_tuning(unroll, ctas_per_sm);
+    return FY_OK;
+}

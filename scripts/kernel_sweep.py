@@ -1,0 +1,56 @@
+"""GPU tuning sweep of the fused Adam kernel (diagnostic, not the bench).
+
+Times fy_adamw_chunk over K chunks of the 13B block size (314,572,800
+params; 8.8 GB of traffic per launch >> L2) for each (unroll, ctas_per_sm)
+and prints achieved GB/s at 28 B/param against MEASURED_PEAKS.json.
+"""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2403_06504_b200 import optim as F  # noqa: E402
+from paper_2403_06504_b200._lib import LIB, check  # noqa: E402
+
+N = 12 * 5120 * 5120
+K = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+dev = torch.device("cuda")
+states = [torch.rand(3 * N, device=dev) * 1e-3 for _ in range(K)]
+grads = [(torch.randn(N, device=dev) * 1e-3).to(torch.bfloat16) for _ in range(K)]
+ws = torch.zeros(F.workspace_floats(), device=dev)
+sq = torch.zeros(1, dtype=torch.float64, device=dev)
+bad = torch.zeros(1, dtype=torch.int32, device=dev)
+hp = F.Hparams()
+results = []
+for unroll in (1, 2, 4, 8):
+    for cps in (0, 1, 2, 3, 4, 6, 8):
+        check(LIB.fy_adamw_tune(unroll, cps))
+        def launch(k):
+            st = states[k]
+            F.adamw_chunk(st[:N], st[N:2 * N], st[2 * N:], grads[k], hp, param_out=grads[k],
+                          grad_sq_sum=sq, workspace=ws, nonfinite=bad)
+        for k in range(K):
+            launch(k)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        reps = 3
+        ev[0].record()
+        for r in range(reps):
+            for k in range(K):
+                launch(k)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / (reps * K)
+        gbs = 28 * N / (ms * 1e-3) / 1e9
+        results.append(dict(unroll=unroll, ctas_per_sm=cps, ms=ms, gbs=gbs, frac=gbs / peak))
+        print(f"unroll={unroll} ctas_per_sm={cps}: {ms:.3f} ms/launch  {gbs:.0f} GB/s  {gbs / peak:.3f} of peak", flush=True)
+check(LIB.fy_adamw_tune(4, 0))
+best = max(results, key=lambda r: r["gbs"])
+print("BEST", json.dumps(best))
+out = ROOT / "gpurun_out" / "kernel_sweep.json"
+out.parent.mkdir(exist_ok=True)
+out.write_text(json.dumps(results, indent=1))
