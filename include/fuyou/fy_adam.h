@@ -108,10 +108,12 @@ fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad
                         double* grad_sq_sum, int accumulate_sq, float* workspace,
                         int* nonfinite_flag, void* stream);
 
-/* Tuning of the fused kernel (diagnostics / sweeps): quads (4 elements) per
- * thread per grid-stride iteration in {1,2,4,8} (default 4) and resident CTAs
- * per SM (0 = occupancy limit). Process-wide. */
-fy_status fy_adamw_tune(int unroll, int ctas_per_sm);
+/* Tuning of the fused kernel (diagnostics / sweeps), process-wide.
+ * path 0: LSU kernel, `unroll` quads (4 elements) per thread per grid-stride
+ *         iteration in {1,2,4,8}, `ctas_per_sm` resident CTAs (0 = occupancy);
+ * path 1: TMA bulk-copy kernel (cp.async.bulk + mbarrier), `unroll` = stages
+ *         in {3,6}. Defaults: the measured best (see profiles/). */
+fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
 
 /* Number of SMs and the launch geometry the kernels use on `device`
  * (diagnostics / roofline bookkeeping). */

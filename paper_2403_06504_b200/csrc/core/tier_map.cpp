@@ -162,8 +162,11 @@ HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRat
     const double head = 1.05;
     hw.bw_gpu = std::max(r.h2d_bps, r.d2h_bps) * head;
     hw.n_ssd = 1;
-    hw.bw_s2c = r.file_read_bps > 0 ? r.file_read_bps * head : 1e15;
-    hw.bw_c2s = r.file_write_bps > 0 ? r.file_write_bps * head : 1e15;
+    // file IO through a virtio / NVMe device cache varies more than copy
+    // engines do: wider headroom keeps the bound a valid necessary condition
+    const double io_head = 1.5;
+    hw.bw_s2c = r.file_read_bps > 0 ? r.file_read_bps * io_head : 1e15;
+    hw.bw_c2s = r.file_write_bps > 0 ? r.file_write_bps * io_head : 1e15;
     hw.cpu_opt_tput = r.optimizer_params_per_s * head;
     hw.gpu_tput = r.compute_flops;
     if (r.gpu_mem) hw.gpu_mem = r.gpu_mem;

@@ -57,8 +57,10 @@ struct Geometry {
 };
 Geometry geometry(int device);
 
-// Tuning knobs of the vector kernel (quads per thread per iteration: 1, 2,
-// 4 or 8; resident CTAs per SM, 0 = occupancy limit). Diagnostics/sweeps.
-void set_tuning(int unroll, int ctas_per_sm);
+// Tuning knobs (diagnostics / sweeps): path 0 = LSU vector kernel with
+// `unroll` quads per thread (1, 2, 4, 8) and `ctas_per_sm` resident CTAs
+// (0 = occupancy limit); path 1 = TMA bulk kernel with `unroll` pipeline
+// stages (3 or 6).
+void set_tuning(int path, int unroll, int ctas_per_sm);
 
 } // namespace fy

@@ -476,18 +476,26 @@ MeasuredRates Engine::calibrate() {
         r.optimizer_params_per_s = n_ / sec;
     }
     if (file_tier_) {
+        // Best of three, writes unsynced exactly as the executor issues them:
+        // the rates must be upper bounds for the roofline check. Requests of
+        // a few MB (smaller than the calibration size) can see device-cache
+        // speedups, hence the extra IO headroom applied in b200_hardware.
         IoRequest w{f_states_->fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
                     &io_error_text_, &io_mu_};
-        const auto t0 = std::chrono::steady_clock::now();
-        run_io(&w);
-        ::fdatasync(f_states_->fd());
-        const auto t1 = std::chrono::steady_clock::now();
         IoRequest rd = w;
         rd.write = false;
-        run_io(&rd);
-        const auto t2 = std::chrono::steady_clock::now();
-        r.file_write_bps = bytes / std::chrono::duration<double>(t1 - t0).count();
-        r.file_read_bps = bytes / std::chrono::duration<double>(t2 - t1).count();
+        double best_w = 1e30, best_r = 1e30;
+        for (int it = 0; it < 3; ++it) {
+            const auto t0 = std::chrono::steady_clock::now();
+            run_io(&w);
+            const auto t1 = std::chrono::steady_clock::now();
+            run_io(&rd);
+            const auto t2 = std::chrono::steady_clock::now();
+            best_w = std::min(best_w, std::chrono::duration<double>(t1 - t0).count());
+            best_r = std::min(best_r, std::chrono::duration<double>(t2 - t1).count());
+        }
+        r.file_write_bps = bytes / best_w;
+        r.file_read_bps = bytes / best_r;
         // restore the block-0 states the calibration write clobbered
         IoRequest fix{f_states_->fd(), h_states_[0], round_up(12 * n_), 0, true, false, &io_error_,
                       &io_error_text_, &io_mu_};

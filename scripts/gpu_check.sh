@@ -7,14 +7,17 @@ mkdir -p $OUT
 nvidia-smi -L > $OUT/${TAG}_gpu.txt 2>&1
 (timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/${TAG}_smoke.log)
 (timeout 900 python -m pytest tests -x -q -m gpu > $OUT/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/${TAG}_pytest_gpu.log)
+if [ "${SWEEP:-0}" = "1" ]; then
+  (timeout 600 python scripts/kernel_sweep.py > $OUT/${TAG}_sweep.log 2>&1; echo "sweep rc=$?" >> $OUT/${TAG}_sweep.log)
+fi
 if [ "${SKIP_BENCH:-0}" != "1" ]; then
   (timeout 900 python bench.py ${BENCH_ARGS:-} > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err; echo "bench rc=$?" >> $OUT/${TAG}_bench.err)
 fi
 if [ "${SKIP_NCU:-0}" != "1" ]; then
-  (timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  (timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:fy:: -c 400 --csv \
      --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e \
      --no-streamed --no-cpu-baseline > $OUT/${TAG}_ncu_launch_run.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/${TAG}_ncu_launch_run.log)
-  (timeout 900 ncu --set full --clock-control none --import-source on -k regex:adamw_vec -s 4 -c 1 \
+  (timeout 900 ncu --set full --clock-control none --import-source on -k regex:adamw_vec -s 4 -c 1 --target-processes all \
      -o $OUT/${TAG}_adamw python bench.py --steps 1 --warmup 1 --layers 6 --no-e2e --no-streamed \
      --no-cpu-baseline > $OUT/${TAG}_ncu_full_run.log 2>&1; echo "ncu-full rc=$?" >> $OUT/${TAG}_ncu_full_run.log)
 fi

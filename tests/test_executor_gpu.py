@@ -53,6 +53,10 @@ def _oracle_check(chunks, ref, s, step=10):
     assert abs(s["optimizer"]["grad_sq_sum"] - sq) <= 1e-5 * sq
 
 
+def _failing(s):
+    return None if s is None else [e for e in s["invariants"] if not e["pass"]]
+
+
 def _inv(s):
     return {e["name"]: (e["pass"], e["detail"]) for e in s["invariants"]}
 
@@ -60,7 +64,7 @@ def _inv(s):
 def test_c1_overlapped_host_tier_matches_oracle(cuda_dev):
     chunks, ref = _chunks(cuda_dev)
     st, s, err = graph_execute(scenario(), {"tier": "host", "compute_rate": RATE}, chunks)
-    assert st == 0, err
+    assert st == 0, (err, _failing(s))
     assert s["all_invariants_pass"], s["invariants"]
     assert s["swap_mismatches"] == 0 and s["swap_checks"] == L  # one checkpoint per block
     pb = s["physical_bytes"]
@@ -73,7 +77,7 @@ def test_c1_overlapped_host_tier_matches_oracle(cuda_dev):
 def test_c1_b128_swapped_layers_round_trip(cuda_dev):
     # b=128: the planner swaps 13 linear_4htoh activations (coefficient 0.139)
     st, s, _, err = execute(scenario(batch=128), {"tier": "host", "compute_rate": RATE})
-    assert st == 0, err
+    assert st == 0, (err, _failing(s))
     assert s["all_invariants_pass"], s["invariants"]
     assert s["swap_checks"] == L + 13 and s["swap_mismatches"] == 0
     assert s["physical_bytes"]["d2h/activations"] == s["reference_bytes"]["link_g2c/activations"]
@@ -86,7 +90,7 @@ def test_c1_file_tier_checkpoints_on_ssd(cuda_dev, tmp_path):
     chunks, ref = _chunks(cuda_dev, seed=100)
     st, s, err = graph_execute(sc, {"tier": "file", "file_dir": str(tmp_path),
                                     "compute_rate": RATE}, chunks)
-    assert st == 0, err
+    assert st == 0, (err, _failing(s))
     assert s["checkpoint_location"] == "ssd"
     assert s["all_invariants_pass"], s["invariants"]
     assert s["swap_mismatches"] == 0 and s["swap_checks"] == L
@@ -102,7 +106,7 @@ def test_pipelined_file_tier_grads_round_trip(cuda_dev, tmp_path):
     st, s, err = graph_execute(scenario(variant="pipelined"),
                                {"tier": "file", "file_dir": str(tmp_path), "compute_rate": RATE},
                                chunks)
-    assert st == 0, err
+    assert st == 0, (err, _failing(s))
     inv = _inv(s)
     assert inv["gradient-ssd-roundtrip"][0], inv["gradient-ssd-roundtrip"]
     assert s["all_invariants_pass"], s["invariants"]
