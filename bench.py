@@ -75,6 +75,7 @@ def parse():
     ap.add_argument("--no-streamed", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streamed-chunks", type=int, default=6)
+    ap.add_argument("--streamed-pieces", type=int, default=4)
     ap.add_argument("--cpu-sample-chunks", type=int, default=2)
     ap.add_argument("--layers", type=int, default=C2["layers"], help="override (debug only)")
     ap.add_argument("--hidden", type=int, default=C2["hidden"], help="override (debug only)")
@@ -266,36 +267,43 @@ def pcie_peaks(torch):
 
 def streamed_phase(torch, F, args, pcie):
     """Out-of-core step over a sample of 65B-shaped chunks, states in pinned
-    host memory. Returns the `streamed` JSON object."""
+    host memory. Each chunk is streamed as `pieces` pipeline units, each with
+    its own [master|m|v] host region, so the copy engines fill and drain the
+    pipeline at piece granularity. Returns the `streamed` JSON object."""
     N = C3["chunk"]
     K = args.streamed_chunks
+    P = args.streamed_pieces
+    n = N // P
+    assert n * P == N and n % 8 == 0
     dev = torch.device("cuda")
     hs, hp_ = [], []
     ptrs = []
-    for k in range(K):
+    for k in range(K * P):
         st = C.c_void_p()
-        F.check(F.LIB.fy_host_alloc(12 * N, C.byref(st)))
+        F.check(F.LIB.fy_host_alloc(12 * n, C.byref(st)))
         pp = C.c_void_p()
-        F.check(F.LIB.fy_host_alloc(2 * N, C.byref(pp)))
+        F.check(F.LIB.fy_host_alloc(2 * n, C.byref(pp)))
         ptrs += [st, pp]
         hs.append(st.value)
         hp_.append(pp.value)
-    # fill host states from the device (fast), per chunk
+    # fill host states from the device (fast), per piece
     grads = []
     gen = torch.Generator(device=dev)
     for k in range(K):
         gen.manual_seed(SEED + 1000 + k)
-        tmp = torch.empty(3 * N, dtype=torch.float32, device=dev)
-        tmp[:N].normal_(0, 0.02, generator=gen)
-        tmp[N:2 * N].normal_(0, 1e-3, generator=gen)
-        tmp[2 * N:].normal_(0, 1e-3, generator=gen).square_()
-        host = torch.from_numpy(np.ctypeslib.as_array((C.c_float * (3 * N)).from_address(hs[k])))
-        host.copy_(tmp)
-        del tmp
         grads.append((torch.randn(N, device=dev, generator=gen) * 1e-3).to(torch.bfloat16))
+        for q in range(P):
+            tmp = torch.empty(3 * n, dtype=torch.float32, device=dev)
+            tmp[:n].normal_(0, 0.02, generator=gen)
+            tmp[n:2 * n].normal_(0, 1e-3, generator=gen)
+            tmp[2 * n:].normal_(0, 1e-3, generator=gen).square_()
+            host = torch.from_numpy(np.ctypeslib.as_array((C.c_float * (3 * n)).from_address(hs[k * P + q])))
+            host.copy_(tmp)
+            del tmp
     torch.cuda.synchronize()
-    pipe = F.optim.ChunkPipeline(N, slots=3, grads_on_host=False, params_to_host=True)
-    chunks = [dict(n=N, h_states=hs[k], grad=grads[k].data_ptr(), h_param=hp_[k]) for k in range(K)]
+    pipe = F.optim.ChunkPipeline(n, slots=4, grads_on_host=False, params_to_host=True)
+    chunks = [dict(n=n, h_states=hs[k * P + q], grad=grads[k].data_ptr() + 2 * n * q,
+                   h_param=hp_[k * P + q]) for k in range(K) for q in range(P)]
     hp = F.optim.Hparams()
     for _ in range(2):
         pipe.step(chunks, hp)
@@ -306,8 +314,7 @@ def streamed_phase(torch, F, args, pcie):
         pipe.step(chunks, hp)
         pipe.wait()
     el = (time.perf_counter() - t0) / reps
-    tim, step_ns = pipe.timings(K)
-    # steady state: from the first D2H start to the last D2H end
+    tim, step_ns = pipe.timings(K * P)
     d2h_busy = sum(t["d2h"][1] - t["d2h"][0] for t in tim) * 1e-9
     h2d_busy = sum(t["h2d"][1] - t["h2d"][0] for t in tim) * 1e-9
     rate = K * N / el
@@ -315,8 +322,8 @@ def streamed_phase(torch, F, args, pcie):
     h2d_gbs = 12 * N * K / el / 1e9
     out = {
         "value": rate, "unit": UNIT,
-        "config": f"{K} x 65B-shaped chunks ({N} params each), states pinned host, grads HBM, "
-                  "bf16 params D2H",
+        "config": f"{K} x 65B-shaped chunks ({N} params each) streamed as {P} pieces each, "
+                  "states pinned host, grads HBM, bf16 params D2H",
         "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
         "d2h_engine_busy_frac": d2h_busy / el, "h2d_engine_busy_frac": h2d_busy / el,
         "roofline": {"bound": "host-link D2H", "achieved": d2h_gbs,
@@ -473,6 +480,40 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt):
     }
 
 
+def iteration_phase(F):
+    """One whole Fuyou iteration of the GPT-2-small-shaped config C1 (b=8,
+    s=1024, a100 preset plan) executed by offsim_execute: every task of the
+    planner's graph on real engines, checked by the unchanged trace
+    invariants. Evidence for SURVEY.md §8 A7/A8/A13/A14."""
+    L = F.LIB
+    P = C.c_void_p
+    L.offsim_scenario_parse.argtypes = [C.c_char_p, C.POINTER(P)]
+    L.offsim_scenario_free.argtypes = [P]
+    L.offsim_execute.argtypes = [P, C.c_char_p, C.POINTER(P), C.POINTER(P)]
+    L.offsim_string_free.argtypes = [P]
+    out = {}
+    for tag, batch in (("c1_b8", 8), ("c1_b128", 128)):
+        sc = json.dumps({"schema_version": 1, "model": {"name": "gpt2-small-shape", "num_layers": 12,
+                         "num_heads": 12, "hidden_dim": 768, "batch_size": batch, "seq_len": 1024},
+                         "hardware": "a100-12ssd", "variant": "overlapped"})
+        h = P()
+        assert L.offsim_scenario_parse(sc.encode(), C.byref(h)) == 0
+        summ = P()
+        st = L.offsim_execute(h, json.dumps({"tier": "host", "compute_rate": 1.4e15}).encode(),
+                              C.byref(summ), None)
+        L.offsim_scenario_free(h)
+        d = json.loads(C.cast(summ, C.c_char_p).value.decode())
+        L.offsim_string_free(summ)
+        out[tag] = {"status": st, "all_invariants_pass": d["all_invariants_pass"],
+                    "executed_makespan_s": d["executed"]["makespan_s"],
+                    "planned_makespan_s": d["planned"]["makespan_s"],
+                    "tasks": d["task_count"], "swap_checks": d["swap_checks"],
+                    "swap_mismatches": d["swap_mismatches"],
+                    "optimizer_kernel_params_per_s": d["optimizer"]["kernel_params_per_s"],
+                    "launches": d["kernel_launches"]}
+    return out
+
+
 # -------------------------------------------------------------------- main
 
 def run_reference(args):
@@ -551,12 +592,20 @@ def main():
     if rank == 0 and world == 1 and not args.no_streamed:
         extra["streamed"] = streamed_phase(torch, F, args, pcie)
 
+    if rank == 0 and world == 1:
+        try:
+            extra["executed_iteration"] = iteration_phase(F)
+        except Exception as e:  # evidence only; never masks the headline
+            extra["executed_iteration"] = f"failed: {e}"
     res = resident_phase(torch, F, args, world, rank, local)
     peak, peak_src = peaks()
     cnt = res["params_per_launch"]
     achieved = BYTES_RESIDENT * cnt / res["mean_launch_s"] / 1e9
     P = args.layers * 12 * args.hidden * args.hidden
     if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,

@@ -113,6 +113,7 @@ struct ExecReport {
     std::uint64_t swap_checks = 0;     // restored buffers verified
     std::uint64_t swap_mismatches = 0; // must be 0
     std::uint32_t kernel_launches = 0;
+    std::string io_engine; // "io_uring" | "pread/pwrite" (file tier)
 };
 
 ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const SwapPlan& plan,

@@ -10,7 +10,18 @@ from pathlib import Path
 
 import numpy as np
 
-_SO = Path(__file__).resolve().parent / "_build" / "liboracle_adamw.so"
+_BUILD = Path(__file__).resolve().parent / "_build"
+
+
+def _has_avx512() -> bool:
+    try:
+        return " avx512f " in (" " + open("/proc/cpuinfo").read().replace("\n", " ") + " ")
+    except OSError:
+        return False
+
+
+_SO = _BUILD / ("liboracle_adamw_avx512.so" if _has_avx512() and (_BUILD / "liboracle_adamw_avx512.so").exists()
+                else "liboracle_adamw.so")
 BF16, FP16, FP32 = 0, 1, 2
 
 

@@ -146,6 +146,7 @@ std::string exec_summary_json(const ExecReport& r) {
         {"swap_checks", r.swap_checks},
         {"swap_mismatches", r.swap_mismatches},
         {"kernel_launches", r.kernel_launches},
+        {"io_engine", r.io_engine},
         {"invariants", checks},
         {"all_invariants_pass", r.invariants.all_pass && r.swap_mismatches == 0},
     };

@@ -1,0 +1,148 @@
+// io_uring IO engine (raw syscalls) with a pread/pwrite fallback.
+#include "io_engine.hpp"
+
+#include <linux/io_uring.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <cerrno>
+#include <cstring>
+#include <vector>
+
+namespace fy {
+
+namespace {
+
+int uring_setup(unsigned entries, io_uring_params* p) {
+    return static_cast<int>(::syscall(__NR_io_uring_setup, entries, p));
+}
+int uring_enter(int fd, unsigned submit, unsigned wait, unsigned flags) {
+    return static_cast<int>(::syscall(__NR_io_uring_enter, fd, submit, wait, flags, nullptr, 0));
+}
+template <typename T>
+T* at(void* base, std::uint32_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+} // namespace
+
+IoEngine::IoEngine(unsigned depth, std::uint64_t piece) : depth_(depth), piece_(piece) {
+    io_uring_params p;
+    std::memset(&p, 0, sizeof p);
+    const int fd = uring_setup(depth, &p);
+    if (fd < 0) return; // refused: fall back to pread/pwrite
+    sq_len_ = p.sq_off.array + p.sq_entries * sizeof(unsigned);
+    cq_len_ = p.cq_off.cqes + p.cq_entries * sizeof(io_uring_cqe);
+    const bool single = (p.features & IORING_FEAT_SINGLE_MMAP) != 0;
+    if (single) sq_len_ = cq_len_ = std::max(sq_len_, cq_len_);
+    sq_ptr_ = ::mmap(nullptr, sq_len_, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd,
+                     IORING_OFF_SQ_RING);
+    if (sq_ptr_ == MAP_FAILED) {
+        ::close(fd);
+        sq_ptr_ = nullptr;
+        return;
+    }
+    cq_ptr_ = single ? sq_ptr_
+                     : ::mmap(nullptr, cq_len_, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd,
+                              IORING_OFF_CQ_RING);
+    sqes_len_ = p.sq_entries * sizeof(io_uring_sqe);
+    sqes_ = ::mmap(nullptr, sqes_len_, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd,
+                   IORING_OFF_SQES);
+    if (cq_ptr_ == MAP_FAILED || sqes_ == MAP_FAILED) {
+        ::close(fd);
+        return;
+    }
+    sq_head_ = at<unsigned>(sq_ptr_, p.sq_off.head);
+    sq_tail_ = at<unsigned>(sq_ptr_, p.sq_off.tail);
+    sq_mask_ = at<unsigned>(sq_ptr_, p.sq_off.ring_mask);
+    sq_array_ = at<unsigned>(sq_ptr_, p.sq_off.array);
+    cq_head_ = at<unsigned>(cq_ptr_, p.cq_off.head);
+    cq_tail_ = at<unsigned>(cq_ptr_, p.cq_off.tail);
+    cq_mask_ = at<unsigned>(cq_ptr_, p.cq_off.ring_mask);
+    cqes_ = at<void>(cq_ptr_, p.cq_off.cqes);
+    depth_ = std::min(depth_, p.sq_entries);
+    ring_fd_ = fd;
+}
+
+IoEngine::~IoEngine() {
+    if (sqes_ && sqes_ != MAP_FAILED) ::munmap(sqes_, sqes_len_);
+    if (cq_ptr_ && cq_ptr_ != MAP_FAILED && cq_ptr_ != sq_ptr_) ::munmap(cq_ptr_, cq_len_);
+    if (sq_ptr_ && sq_ptr_ != MAP_FAILED) ::munmap(sq_ptr_, sq_len_);
+    if (ring_fd_ >= 0) ::close(ring_fd_);
+}
+
+std::string IoEngine::transfer_sync(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset,
+                                    bool write) {
+    std::uint64_t done = 0;
+    while (done < bytes) {
+        char* p = static_cast<char*>(buf) + done;
+        const ssize_t n = write ? ::pwrite(fd, p, bytes - done, static_cast<off_t>(offset + done))
+                                : ::pread(fd, p, bytes - done, static_cast<off_t>(offset + done));
+        if (n < 0 && errno == EINTR) continue;
+        if (n <= 0)
+            return std::string(write ? "pwrite" : "pread") + " failed: " +
+                   (n < 0 ? std::strerror(errno) : "short transfer");
+        done += static_cast<std::uint64_t>(n);
+    }
+    return {};
+}
+
+std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset,
+                               bool write) {
+    if (ring_fd_ < 0) return transfer_sync(fd, buf, bytes, offset, write);
+    const std::uint64_t pieces = (bytes + piece_ - 1) / piece_;
+    auto* sqes = static_cast<io_uring_sqe*>(sqes_);
+    auto* cqes = static_cast<io_uring_cqe*>(cqes_);
+    std::vector<std::uint64_t> short_pieces;
+    std::uint64_t next = 0, inflight = 0, failed_errno = 0;
+    while (next < pieces || inflight > 0) {
+        unsigned queued = 0;
+        unsigned tail = __atomic_load_n(sq_tail_, __ATOMIC_RELAXED);
+        while (next < pieces && inflight + queued < depth_) {
+            const std::uint64_t off = next * piece_;
+            const unsigned idx = tail & *sq_mask_;
+            io_uring_sqe& e = sqes[idx];
+            std::memset(&e, 0, sizeof e);
+            e.opcode = write ? IORING_OP_WRITE : IORING_OP_READ;
+            e.fd = fd;
+            e.addr = reinterpret_cast<std::uint64_t>(static_cast<char*>(buf) + off);
+            e.len = static_cast<std::uint32_t>(std::min(piece_, bytes - off));
+            e.off = offset + off;
+            e.user_data = next;
+            sq_array_[idx] = idx;
+            ++tail;
+            ++queued;
+            ++next;
+        }
+        __atomic_store_n(sq_tail_, tail, __ATOMIC_RELEASE);
+        const int r = uring_enter(ring_fd_, queued, 1, IORING_ENTER_GETEVENTS);
+        if (r < 0 && errno != EINTR) return std::string("io_uring_enter failed: ") + std::strerror(errno);
+        inflight += queued;
+        unsigned head = __atomic_load_n(cq_head_, __ATOMIC_RELAXED);
+        const unsigned ctail = __atomic_load_n(cq_tail_, __ATOMIC_ACQUIRE);
+        while (head != ctail) {
+            const io_uring_cqe& c = cqes[head & *cq_mask_];
+            const std::uint64_t piece_idx = c.user_data;
+            const std::uint64_t want = std::min(piece_, bytes - piece_idx * piece_);
+            if (c.res < 0) failed_errno = static_cast<std::uint64_t>(-c.res);
+            else if (static_cast<std::uint64_t>(c.res) != want) short_pieces.push_back(piece_idx);
+            ++head;
+            --inflight;
+        }
+        __atomic_store_n(cq_head_, head, __ATOMIC_RELEASE);
+    }
+    if (failed_errno)
+        return std::string(write ? "io_uring write" : "io_uring read") + " failed: " +
+               std::strerror(static_cast<int>(failed_errno));
+    for (const std::uint64_t i : short_pieces) { // rare: finish synchronously
+        const std::uint64_t off = i * piece_;
+        const std::string err =
+            transfer_sync(fd, static_cast<char*>(buf) + off, std::min(piece_, bytes - off), offset + off, write);
+        if (!err.empty()) return err;
+    }
+    return {};
+}
+
+} // namespace fy

@@ -1,0 +1,49 @@
+// File-tier IO engine: io_uring on raw syscalls (liburing is not available):
+// submits one large transfer as many fixed-size O_DIRECT reads/writes in
+// flight at once, which is what an NVMe array needs to reach its aggregate
+// bandwidth (the reference's SSD lane is n_ssd devices, hardware.cpp:39-42).
+// Falls back to a pread/pwrite loop when io_uring_setup is refused (old
+// kernel or a sandbox seccomp policy); `engine()` reports which one ran.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+namespace fy {
+
+class IoEngine {
+public:
+    // depth: requests in flight; piece: bytes per request (multiple of 4 KiB)
+    explicit IoEngine(unsigned depth = 32, std::uint64_t piece = 4ull << 20);
+    ~IoEngine();
+    IoEngine(const IoEngine&) = delete;
+    IoEngine& operator=(const IoEngine&) = delete;
+
+    // Transfers `bytes` between buf and fd at `offset`; returns "" on
+    // success or an error message. Thread-compatible (one caller at a time).
+    std::string transfer(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset, bool write);
+
+    const char* engine() const { return ring_fd_ >= 0 ? "io_uring" : "pread/pwrite"; }
+
+private:
+    std::string transfer_sync(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset, bool write);
+
+    int ring_fd_ = -1;
+    unsigned depth_ = 0;
+    std::uint64_t piece_ = 0;
+    // mapped rings
+    void* sq_ptr_ = nullptr;
+    void* cq_ptr_ = nullptr;
+    void* sqes_ = nullptr;
+    std::uint64_t sq_len_ = 0, cq_len_ = 0, sqes_len_ = 0;
+    unsigned* sq_head_ = nullptr;
+    unsigned* sq_tail_ = nullptr;
+    unsigned* sq_mask_ = nullptr;
+    unsigned* sq_array_ = nullptr;
+    unsigned* cq_head_ = nullptr;
+    unsigned* cq_tail_ = nullptr;
+    unsigned* cq_mask_ = nullptr;
+    void* cqes_ = nullptr;
+};
+
+} // namespace fy

@@ -16,6 +16,7 @@
 
 #include "adamw_kernels.cuh"
 #include "pipeline.cuh"
+#include "../core/io_engine.hpp"
 
 #include "offsim/errors.hpp"
 #include "offsim/exec.hpp"
@@ -103,6 +104,7 @@ __global__ void count_mismatch(const std::uint64_t* a, const std::uint64_t* b, s
 // --------------------------------------------------------- file tier
 
 struct IoRequest {
+    fy::IoEngine* io = nullptr;
     int fd = -1;
     void* buf = nullptr;
     std::uint64_t bytes = 0; // rounded to kAlign for O_DIRECT
@@ -116,21 +118,12 @@ struct IoRequest {
 
 void CUDART_CB run_io(void* arg) {
     auto* r = static_cast<IoRequest*>(arg);
-    std::uint64_t done = 0;
-    while (done < r->bytes) {
-        char* p = static_cast<char*>(r->buf) + done;
-        const std::uint64_t left = r->bytes - done;
-        const ssize_t n = r->write ? ::pwrite(r->fd, p, left, static_cast<off_t>(r->offset + done))
-                                   : ::pread(r->fd, p, left, static_cast<off_t>(r->offset + done));
-        if (n < 0 && errno == EINTR) continue;
-        if (n <= 0) {
-            std::lock_guard<std::mutex> lk(*r->error_mu);
-            r->error->store(1);
-            *r->error_text = std::string(r->write ? "pwrite" : "pread") + " failed: " +
-                             (n < 0 ? std::strerror(errno) : "short read");
-            return;
-        }
-        done += static_cast<std::uint64_t>(n);
+    const std::string err = r->io->transfer(r->fd, r->buf, r->bytes, r->offset, r->write);
+    if (!err.empty()) {
+        std::lock_guard<std::mutex> lk(*r->error_mu);
+        r->error->store(1);
+        *r->error_text = err;
+        return;
     }
     if (r->write && r->poison_after) std::memset(r->buf, 0xA5, r->bytes);
 }
@@ -233,6 +226,7 @@ public:
 
     void setup();
     MeasuredRates calibrate();
+    const char* io_engine() const { return io_.engine(); }
     void run(const SimTrace& planned, ExecReport& rep);
 
 private:
@@ -275,7 +269,8 @@ private:
     std::unique_ptr<TierFile> f_states_, f_params_, f_acts_, f_grads_;
     std::vector<std::uint64_t> act_file_off_;
     std::vector<std::uint64_t> ckpt_file_off_;
-    std::vector<std::unique_ptr<IoRequest>> io_;
+    std::vector<std::unique_ptr<IoRequest>> io_reqs_;
+    fy::IoEngine io_;
     std::atomic<int> io_error_{0};
     std::string io_error_text_;
     std::mutex io_mu_;
@@ -411,10 +406,10 @@ void Engine::setup() {
             f_grads_ = std::make_unique<TierFile>(stem + "grads.bin", blocks_ * round_up(param_b), direct);
         // the tier holds the initial states / params before the step
         for (std::uint32_t k = 0; k < blocks_; ++k) {
-            IoRequest w{f_states_->fd(), h_states_[k], round_up(state_b), k * round_up(state_b), true,
+            IoRequest w{&io_, f_states_->fd(), h_states_[k], round_up(state_b), k * round_up(state_b), true,
                         false, &io_error_, &io_error_text_, &io_mu_};
             run_io(&w);
-            IoRequest wp{f_params_->fd(), h_params_[k], round_up(param_b), k * round_up(param_b), true,
+            IoRequest wp{&io_, f_params_->fd(), h_params_[k], round_up(param_b), k * round_up(param_b), true,
                          false, &io_error_, &io_error_text_, &io_mu_};
             run_io(&wp);
         }
@@ -480,7 +475,7 @@ MeasuredRates Engine::calibrate() {
         // the rates must be upper bounds for the roofline check. Requests of
         // a few MB (smaller than the calibration size) can see device-cache
         // speedups, hence the extra IO headroom applied in b200_hardware.
-        IoRequest w{f_states_->fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
+        IoRequest w{&io_, f_states_->fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
                     &io_error_text_, &io_mu_};
         IoRequest rd = w;
         rd.write = false;
@@ -497,7 +492,7 @@ MeasuredRates Engine::calibrate() {
         r.file_write_bps = bytes / best_w;
         r.file_read_bps = bytes / best_r;
         // restore the block-0 states the calibration write clobbered
-        IoRequest fix{f_states_->fd(), h_states_[0], round_up(12 * n_), 0, true, false, &io_error_,
+        IoRequest fix{&io_, f_states_->fd(), h_states_[0], round_up(12 * n_), 0, true, false, &io_error_,
                       &io_error_text_, &io_mu_};
         run_io(&fix);
         if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
@@ -535,9 +530,9 @@ void Engine::issue(const Task& t, ExecReport& rep) {
     };
     auto file = [&](const TierFile& f, void* buf, std::uint64_t bytes, std::uint64_t off, bool write,
                     bool poison) {
-        io_.push_back(std::make_unique<IoRequest>(IoRequest{f.fd(), buf, round_up(bytes), off, write,
+        io_reqs_.push_back(std::make_unique<IoRequest>(IoRequest{&io_, f.fd(), buf, round_up(bytes), off, write,
                                                             poison, &io_error_, &io_error_text_, &io_mu_}));
-        check_cuda(cudaLaunchHostFunc(s, run_io, io_.back().get()), "host io");
+        check_cuda(cudaLaunchHostFunc(s, run_io, io_reqs_.back().get()), "host io");
         phys(write ? "file_write" : "file_read", bytes);
     };
 
@@ -709,6 +704,7 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
 
     Engine eng(model, plan, rep.graph, options, chunks);
     eng.setup();
+    if (options.tier == StateTier::file) rep.io_engine = eng.io_engine();
     MeasuredRates rates = eng.calibrate();
     if (rates.compute_flops <= 0) rates.compute_flops = hw.gpu_tput;
     rep.hw_exec = b200_hardware(hw, rates);

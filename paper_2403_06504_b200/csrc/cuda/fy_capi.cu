@@ -202,7 +202,8 @@ extern "C" fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm) {
     if (path != 0 && path != 1) return fail(FY_ERR_CONFIG, "path must be 0 (LSU) or 1 (TMA bulk)");
     if (path == 0 && unroll != 1 && unroll != 2 && unroll != 4 && unroll != 8)
         return fail(FY_ERR_CONFIG, "unroll must be 1, 2, 4 or 8");
-    if (path == 1 && unroll != 3 && unroll != 6) return fail(FY_ERR_CONFIG, "stages must be 3 or 6");
+    if (path == 1 && (unroll < 2 || unroll > 6 || unroll == 5))
+        return fail(FY_ERR_CONFIG, "stages must be 2, 3, 4 or 6");
     if (ctas_per_sm < 0 || ctas_per_sm > 32) return fail(FY_ERR_CONFIG, "ctas_per_sm out of range");
     fy::set_tuning(path, unroll, ctas_per_sm);
     return FY_OK;

@@ -17,7 +17,7 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   (timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:fy:: -c 400 --csv \
      --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e \
      --no-streamed --no-cpu-baseline > $OUT/${TAG}_ncu_launch_run.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/${TAG}_ncu_launch_run.log)
-  (timeout 900 ncu --set full --clock-control none --import-source on -k regex:adamw_vec -s 4 -c 1 --target-processes all \
+  (timeout 900 ncu --set full --clock-control none --import-source on -k regex:adamw_bulk -s 4 -c 1 --target-processes all \
      -o $OUT/${TAG}_adamw python bench.py --steps 1 --warmup 1 --layers 6 --no-e2e --no-streamed \
      --no-cpu-baseline > $OUT/${TAG}_ncu_full_run.log 2>&1; echo "ncu-full rc=$?" >> $OUT/${TAG}_ncu_full_run.log)
 fi
