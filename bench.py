@@ -77,6 +77,7 @@ def parse():
     ap.add_argument("--streamed-chunks", type=int, default=6)
     ap.add_argument("--streamed-pieces", type=int, default=4)
     ap.add_argument("--cpu-sample-chunks", type=int, default=2)
+    ap.add_argument("--no-swap-sweep", action="store_true")
     ap.add_argument("--layers", type=int, default=C2["layers"], help="override (debug only)")
     ap.add_argument("--hidden", type=int, default=C2["hidden"], help="override (debug only)")
     return ap.parse_args()
@@ -514,6 +515,74 @@ def iteration_phase(F):
     return out
 
 
+def swap_sweep_phase(F, budget_cpu=8e9, budget_ssd=2e9):
+    """BASELINE config 5: activation swap GPU->host(->SSD) bandwidth sweep,
+    13B shape, s=2048, b in {8,16,32,64}, swap amounts chosen by the
+    unchanged planner (a100 preset; coefficients 0/0/1/1, checkpoints on
+    CPU). Executes the swap-only subgraph (offsim_execute swap_only) on a
+    bounded number of blocks (host RAM / disk), once with the planner's
+    placement (GPU->pinned host->GPU) and once forcing SSD placement
+    (GPU->host->file->host->GPU, O_DIRECT io_uring). Per-leg GB/s from the
+    real trace (bytes / busy time of the lane)."""
+    L = F.LIB
+    P = C.c_void_p
+    L.offsim_scenario_parse.argtypes = [C.c_char_p, C.POINTER(P)]
+    L.offsim_scenario_free.argtypes = [P]
+    L.offsim_plan.argtypes = [P, C.POINTER(P)]
+    L.offsim_execute.argtypes = [P, C.c_char_p, C.POINTER(P), C.POINTER(P)]
+    L.offsim_string_free.argtypes = [P]
+    rows = []
+    h, s_len = 5120, 2048
+    for b in (8, 16, 32, 64):
+        sc = json.dumps({"schema_version": 1, "model": {"preset": "gpt3-13b", "batch_size": b,
+                                                        "seq_len": s_len},
+                         "hardware": "a100-12ssd", "variant": "overlapped"})
+        hnd = P()
+        assert L.offsim_scenario_parse(sc.encode(), C.byref(hnd)) == 0
+        rep = P()
+        assert L.offsim_plan(hnd, C.byref(rep)) == 0
+        plan = json.loads(C.cast(rep, C.c_char_p).value.decode())["plan"]
+        L.offsim_string_free(rep)
+        coef = plan["swap_coefficient"]
+        per_block = b * s_len * h * (1 + 9 * coef)  # checkpoint + swapped activations (act_elem=1)
+        for placement, budget in (("auto", budget_cpu), ("ssd", budget_ssd)):
+            blocks = int(max(1, min(40, budget // per_block)))
+            opts = {"tier": "file" if placement == "ssd" else "host", "swap_only": True,
+                    "max_blocks": blocks, "placement": placement, "file_dir": "/tmp/offsim_swap"}
+            summ = P()
+            st = L.offsim_execute(hnd, json.dumps(opts).encode(), C.byref(summ), None)
+            d = json.loads(C.cast(summ, C.c_char_p).value.decode()) if summ.value else {}
+            if summ.value:
+                L.offsim_string_free(summ)
+            busy = d.get("executed", {}).get("busy_s", {})
+            pb = d.get("physical_bytes", {})
+            legs = {}
+            for leg, lane, key in (("gpu_to_host", "link_g2c", "d2h/activations"),
+                                   ("host_to_gpu", "link_c2g", "h2d/activations"),
+                                   ("host_to_ssd", "link_ssd", "file_write/activations"),
+                                   ("ssd_to_host", "link_ssd", "file_read/activations")):
+                if pb.get(key):
+                    legs[leg] = {"bytes": pb[key]}
+            if "host_to_ssd" in legs:  # the SSD lane is simplex: split its busy time by bytes
+                tot = legs["host_to_ssd"]["bytes"] + legs["ssd_to_host"]["bytes"]
+                for leg in ("host_to_ssd", "ssd_to_host"):
+                    legs[leg]["busy_s"] = busy.get("link_ssd", 0) * legs[leg]["bytes"] / tot
+            for leg, lane in (("gpu_to_host", "link_g2c"), ("host_to_gpu", "link_c2g")):
+                if leg in legs:
+                    legs[leg]["busy_s"] = busy.get(lane, 0)
+            for v in legs.values():
+                v["gbs"] = v["bytes"] / v["busy_s"] / 1e9 if v.get("busy_s") else None
+            rows.append({"batch": b, "placement": placement, "status": st,
+                         "swap_coefficient": coef, "swapped_layers": plan["swapped_layer_count"],
+                         "d_f_bytes": plan["d_f_bytes"], "checkpoint_location": d.get("checkpoint_location"),
+                         "executed_blocks": blocks, "makespan_s": d.get("executed", {}).get("makespan_s"),
+                         "legs": legs, "all_invariants_pass": d.get("all_invariants_pass"),
+                         "swap_checks": d.get("swap_checks"), "swap_mismatches": d.get("swap_mismatches"),
+                         "io_engine": d.get("io_engine")})
+        L.offsim_scenario_free(hnd)
+    return rows
+
+
 # -------------------------------------------------------------------- main
 
 def run_reference(args):
@@ -597,6 +666,11 @@ def main():
             extra["executed_iteration"] = iteration_phase(F)
         except Exception as e:  # evidence only; never masks the headline
             extra["executed_iteration"] = f"failed: {e}"
+        if not args.no_swap_sweep:
+            try:
+                extra["swap_sweep"] = swap_sweep_phase(F)
+            except Exception as e:
+                extra["swap_sweep"] = f"failed: {e}"
     res = resident_phase(torch, F, args, world, rank, local)
     peak, peak_src = peaks()
     cnt = res["params_per_launch"]

@@ -68,6 +68,11 @@ struct ExecOptions {
     AdamHyper adam;
     std::uint64_t seed = 0;         // synthetic states / grads / activations
     bool verify_swaps = true;       // checksum every restored activation
+    // Activation-swap sweep mode (BASELINE config 5): execute only the
+    // activation / checkpoint transfers (swap_subgraph) of blocks < max_blocks
+    // (0 = all blocks).
+    bool swap_only = false;
+    std::uint32_t max_blocks = 0;
 };
 
 // Caller-provided optimizer states for chunk (block) k: pinned host
@@ -85,6 +90,11 @@ struct ChunkBuffers {
 // slot m % state_slots; the slot-reuse edge is part of the mapped graph.
 TaskGraph map_graph_for_b200(const TaskGraph& graph, StateTier tier,
                              std::uint32_t state_slots = 3);
+
+// The activation-swap path of a (mapped) graph: every task with payload
+// activations whose block index is < max_blocks (0 = all), dependencies
+// restricted to the kept tasks (the swap-out -> [file] -> restore chains).
+TaskGraph swap_subgraph(const TaskGraph& graph, std::uint32_t max_blocks);
 
 // HardwareConfig describing the B200 box for the mapped graph's DES order
 // and invariant checks (measured rates override the preset's).

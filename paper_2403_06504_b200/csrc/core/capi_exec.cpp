@@ -24,7 +24,8 @@ namespace {
 struct ParsedOptions {
     ExecOptions exec;
     bool dry_run = false;
-    std::string variant; // optional override
+    std::string variant;             // optional override
+    std::string placement = "auto";  // checkpoint placement: auto | cpu | ssd
 };
 
 ParsedOptions parse_options(const char* text) {
@@ -39,7 +40,8 @@ ParsedOptions parse_options(const char* text) {
     if (!doc.is_object()) throw ConfigError("exec options must be an object");
     static const std::set<std::string> keys = {"device", "tier", "file_dir", "direct_io",
                                                "compute_rate", "state_slots", "seed",
-                                               "verify_swaps", "adam", "dry_run", "variant"};
+                                               "verify_swaps", "adam", "dry_run", "variant",
+                                               "swap_only", "max_blocks", "placement"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -57,6 +59,11 @@ ParsedOptions parse_options(const char* text) {
         o.verify_swaps = doc.value("verify_swaps", o.verify_swaps);
         out.dry_run = doc.value("dry_run", false);
         out.variant = doc.value("variant", std::string());
+        o.swap_only = doc.value("swap_only", o.swap_only);
+        o.max_blocks = doc.value("max_blocks", o.max_blocks);
+        out.placement = doc.value("placement", out.placement);
+        if (out.placement != "auto" && out.placement != "cpu" && out.placement != "ssd")
+            throw ConfigError("exec options: placement must be 'auto', 'cpu' or 'ssd'");
         if (doc.contains("adam")) {
             const json& a = doc.at("adam");
             static const std::set<std::string> akeys = {"lr", "beta1", "beta2", "eps", "weight_decay",
@@ -155,11 +162,25 @@ std::string exec_summary_json(const ExecReport& r) {
 
 namespace {
 
+// The unchanged planner; `placement` only overrides the all-or-nothing
+// checkpoint placement input (runner.cpp:90-106), e.g. to force the
+// GPU->host->SSD leg of the swap path.
+SwapPlan plan_with_placement(const Scenario& s, const std::string& placement) {
+    if (placement == "auto") return plan_for_scenario(s);
+    PlannerOptions o;
+    o.mode = s.planner_mode;
+    o.fixed_d_f_bytes = s.planner_value;
+    o.fixed_coefficient = s.planner_value;
+    o.checkpoints_on_ssd = placement == "ssd";
+    return plan_swaps(s.model, s.hardware, o);
+}
+
 // Dry run: the mapped graph and its DES on nominal B200 rates (no GPU).
 std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVariant v) {
-    const SwapPlan plan = plan_for_scenario(s);
+    const SwapPlan plan = plan_with_placement(s, po.placement);
     const TaskGraph ref = build_schedule(s.model, s.hardware, plan, v);
-    const TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots);
+    TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots);
+    if (po.exec.swap_only) mapped = swap_subgraph(mapped, po.exec.max_blocks);
     MeasuredRates nominal;
     nominal.h2d_bps = nominal.d2h_bps = 55e9;
     nominal.file_read_bps = nominal.file_write_bps = po.exec.tier == StateTier::file ? 2e9 : 0.0;
@@ -212,7 +233,7 @@ offsim_status run_exec(const Scenario& s, const char* opts_json,
         if (trace_out) *trace_out = nullptr;
         return OFFSIM_OK;
     }
-    const SwapPlan plan = plan_for_scenario(sv);
+    const SwapPlan plan = plan_with_placement(sv, po.placement);
     const ExecReport rep = execute(sv.model, sv.hardware, plan, v, po.exec, chunks);
     const std::string summary = exec_summary_json(rep);
     *summary_out = capi::copy_out(summary);

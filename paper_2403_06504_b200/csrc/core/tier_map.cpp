@@ -153,6 +153,28 @@ TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t 
     return out;
 }
 
+TaskGraph swap_subgraph(const TaskGraph& in, std::uint32_t max_blocks) {
+    TaskGraph out;
+    out.header = in.header;
+    out.initial_mem = in.initial_mem;
+    std::vector<std::uint32_t> remap(in.tasks.size(), 0xffffffffu);
+    for (const Task& src : in.tasks) {
+        if (src.payload != Payload::activations) continue;
+        // names: "<phase> <what> b<k>[ <kind>]"
+        const std::size_t b = src.name.find(" b", src.name.find(' ') + 1);
+        const std::uint32_t blk = static_cast<std::uint32_t>(std::stoul(src.name.substr(b + 2)));
+        if (max_blocks && blk >= max_blocks) continue;
+        Task t = src;
+        t.id = static_cast<std::uint32_t>(out.tasks.size());
+        t.deps.clear();
+        for (const std::uint32_t d : src.deps)
+            if (remap[d] != 0xffffffffu) t.deps.push_back(remap[d]);
+        remap[src.id] = t.id;
+        out.tasks.push_back(std::move(t));
+    }
+    return out;
+}
+
 HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRates& r) {
     // Rates are upper bounds of what the engines delivered (measured burst
     // x 1.05), so the unchanged roofline-lower-bound check stays a valid

@@ -246,6 +246,8 @@ private:
     std::vector<bool> swapped_;
     std::uint64_t ckpt_bytes_ = 0;
     bool file_tier_ = false;
+    bool has_update_ = false;
+    bool has_weights_ = false;
 
     cudaStream_t streams_[5] = {};
     std::vector<cudaEvent_t> events_;
@@ -313,11 +315,21 @@ void Engine::setup() {
 
     const std::uint64_t state_b = 12 * n_, param_b = 2 * n_;
     const std::uint64_t seed = opt_.seed * 0x9e3779b97f4a7c15ull + 17;
-    // optimizer states + params (host), grads (device)
-    h_states_.resize(blocks_);
-    h_params_.resize(blocks_);
-    d_grads_.resize(blocks_);
-    for (std::uint32_t k = 0; k < blocks_; ++k) {
+    // Allocate only what the executed graph touches (a swap-only subgraph
+    // needs no optimizer state at all).
+    std::vector<bool> act_used(layers_.size(), false), ckpt_used(blocks_, false);
+    for (const Task& t : g_.tasks) {
+        if (t.kind == TaskKind::optimizer_update) has_update_ = true;
+        const Parsed p = parse_name(t.name);
+        if (p.what == "p_c2g" || p.what == "p_s2c") has_weights_ = true;
+        if (p.what.rfind("act_", 0) == 0) act_used[4ull * p.block + p.layer] = true;
+        if (p.what.rfind("ckpt_", 0) == 0) ckpt_used[p.block] = true;
+    }
+    const bool need_chunks = has_update_ || has_weights_;
+    h_states_.assign(blocks_, nullptr);
+    h_params_.assign(blocks_, nullptr);
+    d_grads_.assign(blocks_, nullptr);
+    for (std::uint32_t k = 0; k < blocks_ && need_chunks; ++k) {
         if (user_ && (*user_)[k].host_states) {
             h_states_[k] = (*user_)[k].host_states;
             h_params_[k] = (*user_)[k].host_params;
@@ -336,7 +348,7 @@ void Engine::setup() {
         }
     }
     // synthetic host states when not provided: generate on the device, copy
-    if (!(user_ && (*user_)[0].host_states)) {
+    if (need_chunks && !(user_ && (*user_)[0].host_states)) {
         Device tmp(state_b);
         for (std::uint32_t k = 0; k < blocks_; ++k) {
             fill_states<<<592, 256>>>(static_cast<float*>(tmp.p), n_, seed + 7 * k);
@@ -344,13 +356,16 @@ void Engine::setup() {
             std::memset(h_params_[k], 0, param_b);
         }
     }
-    const std::uint32_t slots = std::max<std::uint32_t>(2, opt_.state_slots);
-    for (std::uint32_t s = 0; s < slots; ++s) slots_.emplace_back(state_b);
-
-    std::uint64_t max_w = 0;
-    for (const LayerProfile& l : layers_) max_w = std::max(max_w, l.param_bytes);
-    wscratch_[0] = Device(max_w);
-    wscratch_[1] = Device(max_w);
+    if (has_update_) {
+        const std::uint32_t slots = std::max<std::uint32_t>(2, opt_.state_slots);
+        for (std::uint32_t s = 0; s < slots; ++s) slots_.emplace_back(state_b);
+    }
+    if (has_weights_) {
+        std::uint64_t max_w = 0;
+        for (const LayerProfile& l : layers_) max_w = std::max(max_w, l.param_bytes);
+        wscratch_[0] = Device(max_w);
+        wscratch_[1] = Device(max_w);
+    }
 
     // activation / checkpoint units: device originals (pattern), device
     // restore targets, pinned host landing buffers
@@ -358,22 +373,26 @@ void Engine::setup() {
     act_restore_.resize(layers_.size());
     act_host_.resize(layers_.size());
     for (std::size_t i = 0; i < layers_.size(); ++i) {
-        if (!swapped_[i]) continue;
+        if (!swapped_[i] || !act_used[i]) continue;
         const std::uint64_t b = round_up(layers_[i].act_bytes);
         act_dev_[i] = Device(b);
         act_restore_[i] = Device(b);
         act_host_[i] = Pinned(b);
         fill_pattern<<<296, 256>>>(static_cast<std::uint64_t*>(act_dev_[i].p), b / 8, seed ^ (i + 1));
     }
+    ckpt_dev_.resize(blocks_);
+    ckpt_restore_.resize(blocks_);
+    ckpt_host_.resize(blocks_);
     for (std::uint32_t k = 0; k < blocks_; ++k) {
+        if (!ckpt_used[k]) continue;
         const std::uint64_t b = round_up(ckpt_bytes_);
-        ckpt_dev_.emplace_back(b);
-        ckpt_restore_.emplace_back(b);
-        ckpt_host_.emplace_back(b);
-        fill_pattern<<<296, 256>>>(static_cast<std::uint64_t*>(ckpt_dev_.back().p), b / 8,
+        ckpt_dev_[k] = Device(b);
+        ckpt_restore_[k] = Device(b);
+        ckpt_host_[k] = Pinned(b);
+        fill_pattern<<<296, 256>>>(static_cast<std::uint64_t*>(ckpt_dev_[k].p), b / 8,
                                    seed ^ (0xc0ffee00ull + k));
     }
-    if (g_.header.variant != ScheduleVariant::overlapped)
+    if (g_.header.variant != ScheduleVariant::overlapped && has_update_)
         for (std::uint32_t k = 0; k < blocks_; ++k) grad_host_.emplace_back(round_up(param_b));
 
     workspace_ = Device(sizeof(float) * fy::kWorkspaceFloats);
@@ -388,8 +407,11 @@ void Engine::setup() {
         ::mkdir(opt_.file_dir.c_str(), 0700);
         const bool direct = opt_.direct_io && model_.hidden_dim % 64 == 0;
         const std::string stem = opt_.file_dir + "/offsim_" + std::to_string(::getpid()) + "_";
-        f_states_ = std::make_unique<TierFile>(stem + "states.bin", blocks_ * round_up(state_b), direct);
-        f_params_ = std::make_unique<TierFile>(stem + "params.bin", blocks_ * round_up(param_b), direct);
+        const bool chunks = has_update_ || has_weights_;
+        f_states_ = std::make_unique<TierFile>(stem + "states.bin",
+                                               chunks ? blocks_ * round_up(state_b) : kAlign, direct);
+        f_params_ = std::make_unique<TierFile>(stem + "params.bin",
+                                               chunks ? blocks_ * round_up(param_b) : kAlign, direct);
         std::uint64_t off = 0;
         act_file_off_.assign(layers_.size(), 0);
         for (std::size_t i = 0; i < layers_.size(); ++i)
@@ -405,7 +427,7 @@ void Engine::setup() {
         if (!grad_host_.empty())
             f_grads_ = std::make_unique<TierFile>(stem + "grads.bin", blocks_ * round_up(param_b), direct);
         // the tier holds the initial states / params before the step
-        for (std::uint32_t k = 0; k < blocks_; ++k) {
+        for (std::uint32_t k = 0; k < blocks_ && chunks; ++k) {
             IoRequest w{&io_, f_states_->fd(), h_states_[k], round_up(state_b), k * round_up(state_b), true,
                         false, &io_error_, &io_error_text_, &io_mu_};
             run_io(&w);
@@ -443,7 +465,8 @@ MeasuredRates Engine::calibrate() {
         }
         return best * 1e-3;
     };
-    void* slot = slots_[0].p;
+    Device probe(bytes);
+    void* slot = probe.p;
     r.h2d_bps = bytes / timed(lane_stream(ResourceId::link_c2g), [&](cudaStream_t s) {
                     check_cuda(cudaMemcpyAsync(slot, h.p, bytes, cudaMemcpyHostToDevice, s), "h2d");
                 });
@@ -451,7 +474,8 @@ MeasuredRates Engine::calibrate() {
                     check_cuda(cudaMemcpyAsync(h.p, slot, bytes, cudaMemcpyDeviceToHost, s), "d2h");
                 });
     // fused kernel rate on a scratch copy (does not touch the real states)
-    {
+    r.optimizer_params_per_s = 1e12; // no optimizer task: the lane stays empty
+    if (has_update_) {
         Device st(12 * n_), gr(2 * n_);
         fill_states<<<592, 256>>>(static_cast<float*>(st.p), n_, 1);
         fill_grads<<<592, 256>>>(static_cast<std::uint16_t*>(gr.p), n_, 2);
@@ -492,9 +516,11 @@ MeasuredRates Engine::calibrate() {
         r.file_write_bps = bytes / best_w;
         r.file_read_bps = bytes / best_r;
         // restore the block-0 states the calibration write clobbered
-        IoRequest fix{&io_, f_states_->fd(), h_states_[0], round_up(12 * n_), 0, true, false, &io_error_,
-                      &io_error_text_, &io_mu_};
-        run_io(&fix);
+        if (h_states_[0]) {
+            IoRequest fix{&io_, f_states_->fd(), h_states_[0], round_up(12 * n_), 0, true, false,
+                          &io_error_, &io_error_text_, &io_mu_};
+            run_io(&fix);
+        }
         if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
     }
     r.compute_flops = opt_.compute_rate > 0 ? opt_.compute_rate : 0.0;
@@ -696,11 +722,15 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
                    ScheduleVariant variant, const ExecOptions& options,
                    const std::vector<ChunkBuffers>* chunks) {
     ExecReport rep;
-    const TaskGraph reference = build_schedule(model, hw, plan, variant);
+    TaskGraph reference = build_schedule(model, hw, plan, variant);
+    rep.graph = map_graph_for_b200(reference, options.tier, std::max<std::uint32_t>(2, options.state_slots));
+    if (options.swap_only) {
+        reference = swap_subgraph(reference, options.max_blocks);
+        rep.graph = swap_subgraph(rep.graph, options.max_blocks);
+    }
     for (const Task& t : reference.tasks)
         if (t.kind == TaskKind::transfer)
             rep.reference_bytes[std::string(to_string(t.resource)) + "/" + to_string(t.payload)] += t.work;
-    rep.graph = map_graph_for_b200(reference, options.tier, std::max<std::uint32_t>(2, options.state_slots));
 
     Engine eng(model, plan, rep.graph, options, chunks);
     eng.setup();

@@ -62,3 +62,21 @@ def test_slot_edges_and_bad_options():
     assert st == 2 and "colour" in err
     st, _, _, err = execute(C1, {"dry_run": True, "tier": "tape"})
     assert st == 2
+
+
+def test_swap_only_subgraph_c5():
+    # BASELINE config 5 at b=32 (coefficient 1, all 160 layers swapped):
+    # the swap path of 2 blocks = 2 checkpoints + 8 activations, out and back
+    sc = scenario(40, 40, 5120, 32, 2048, name="gpt3-13b")
+    st, s, _, err = execute(sc, {"dry_run": True, "swap_only": True, "max_blocks": 2})
+    assert st == 0, err
+    assert s["all_invariants_pass"], s["invariants"]
+    assert s["task_count"] == 2 * (2 + 8)  # g2c + c2g per unit (cpu placement)
+    per_block = 32 * 2048 * 5120 * 10
+    assert s["mapped_bytes"]["link_g2c/activations"] == 2 * per_block
+    assert s["mapped_bytes"]["link_c2g/activations"] == 2 * per_block
+    st, s, _, err = execute(sc, {"dry_run": True, "swap_only": True, "max_blocks": 2,
+                                 "placement": "ssd", "tier": "file"})
+    assert st == 0, err
+    assert s["task_count"] == 4 * (2 + 8)  # + c2s and s2c legs
+    assert s["mapped_bytes"]["link_ssd/activations"] == 2 * 2 * per_block
