@@ -427,56 +427,70 @@ def resident_phase(torch, F, args, world, rank, local):
         "nonfinite": int(bad.item()),
     }
 
-    if not args.no_e2e and world == 1:
-        res["e2e"] = e2e_phase(torch, F, args, states, slice_pad, cnt)
+    if not args.no_e2e:
+        res["e2e"] = e2e_phase(torch, F, args, states, slice_pad, cnt, world, full)
     del states, grads, full
     torch.cuda.empty_cache()
     return res
 
 
-def e2e_phase(torch, F, args, states, slice_pad, cnt):
-    """Same step through fy_pipeline_* with host grads in / host params out."""
+def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
+    """Same step through fy_pipeline_* with host grads in / host params out.
+    N>1: each rank streams its own slice (padded to slice_pad) and the
+    updated bf16 slices are all-gathered on the device after each step; the
+    time is the max over ranks."""
+    import torch.distributed as dist
     L = len(states)
+    n = slice_pad
     hbuf = []
     for k in range(L):
         p = C.c_void_p()
-        F.check(F.LIB.fy_host_alloc(2 * cnt, C.byref(p)))
+        F.check(F.LIB.fy_host_alloc(2 * n, C.byref(p)))
         hbuf.append(p)
     # initial host grads: bf16 ~ 1e-3 (0x3A83)
     for p in hbuf:
-        arr = np.ctypeslib.as_array((C.c_uint16 * cnt).from_address(p.value))
+        arr = np.ctypeslib.as_array((C.c_uint16 * n).from_address(p.value))
         arr[:] = 0x3A83
-    pipe = F.optim.ChunkPipeline(cnt, slots=3, grads_on_host=True, params_to_host=True,
+    pipe = F.optim.ChunkPipeline(n, slots=3, grads_on_host=True, params_to_host=True,
                                  states_on_device=True)
-    # states tensors are [master|m|v] padded to slice_pad; the pipeline wants
-    # [master|m|v] contiguous at stride n: use n = slice_pad when unpadded.
-    assert slice_pad == cnt, "e2e runs at N=1 (no shard padding)"
-    chunks = [dict(n=cnt, h_states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value)
+    chunks = [dict(n=n, h_states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value)
               for k in range(L)]
+    staging = torch.empty(n, dtype=torch.bfloat16, device="cuda") if world > 1 else None
     hp = F.optim.Hparams()
+
+    def step(i):
+        hp.step = i
+        pipe.step(chunks, hp, want_grad_norm=True)
+        pipe.wait()
+        if world > 1:  # assemble the full bf16 params on every rank (NVLink)
+            for k in range(L):
+                host = torch.from_numpy(np.ctypeslib.as_array(
+                    (C.c_int16 * n).from_address(hbuf[k].value))).view(torch.bfloat16)
+                staging.copy_(host, non_blocking=True)
+                dist.all_gather_into_tensor(full[k], staging)
+            torch.cuda.synchronize()
+
     for w in range(args.warmup):
-        hp.step = 1000 + w
-        pipe.step(chunks, hp, want_grad_norm=True)
-        pipe.wait()
+        step(1000 + w)
     torch.cuda.synchronize()
+    barrier(world)
     t0 = time.perf_counter()
-    for s in range(args.steps):
-        hp.step = 2000 + s
-        pipe.step(chunks, hp, want_grad_norm=True)
-        pipe.wait()
+    for i in range(args.steps):
+        step(2000 + i)
     el = time.perf_counter() - t0
-    tim, step_ns = pipe.timings(L)
+    el = max_over_ranks(el, world)
     pipe.close()
     for p in hbuf:
         F.check(F.LIB.fy_host_free(p))
-    P = L * cnt
+    P = args.layers * 12 * args.hidden * args.hidden  # whole-job params per step
     return {
         "value": args.steps * P / el, "unit": UNIT,
-        "h2d_bytes_per_step": 2 * P, "d2h_bytes_per_step": 2 * P,
+        "h2d_bytes_per_step": 2 * L * n * world, "d2h_bytes_per_step": 2 * L * n * world,
         "ms_per_step": el / args.steps * 1e3,
-        "link_gbs_each_way": 2 * P * args.steps / el / 1e9,
+        "link_gbs_each_way": 2 * L * n * args.steps / el / 1e9,
         "path": "fy_pipeline_step (C ABI): host bf16 grads H2D -> fused AdamW on HBM-resident "
-                "states -> bf16 params D2H into the same host buffer; wall clock",
+                "states -> bf16 params D2H into the same host buffer; wall clock"
+                + ("; + NCCL all-gather of the bf16 slices" if world > 1 else ""),
         "launches": args.steps * L * 2,
     }
 

@@ -14,11 +14,19 @@ if [ "${SKIP_BENCH:-0}" != "1" ]; then
   (timeout 900 python bench.py ${BENCH_ARGS:-} > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err; echo "bench rc=$?" >> $OUT/${TAG}_bench.err)
 fi
 if [ "${SKIP_NCU:-0}" != "1" ]; then
-  (timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:fy:: -c 400 --csv \
+  (timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'adamw|reduce_partials|grad_stats' -c 400 --csv \
      --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e \
-     --no-streamed --no-cpu-baseline > $OUT/${TAG}_ncu_launch_run.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/${TAG}_ncu_launch_run.log)
+     --no-streamed --no-cpu-baseline --no-swap-sweep > $OUT/${TAG}_ncu_launch_run.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/${TAG}_ncu_launch_run.log)
+  # hardware-counter sections only: the SASS-patching sections (SourceCounters,
+  # InstructionStats) instrument the TMA kernel's mbarrier spin-waits and
+  # inflate both its duration and its DRAM traffic
+  (timeout 900 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section MemoryWorkloadAnalysis_Tables \
+     --section LaunchStats --section Occupancy --section SchedulerStats --section WarpStateStats \
+     --section ComputeWorkloadAnalysis --clock-control none -k regex:adamw_bulk -s 4 -c 1 \
+     -o $OUT/${TAG}_adamw_hw python bench.py --steps 1 --warmup 1 --layers 6 --no-e2e --no-streamed \
+     --no-cpu-baseline --no-swap-sweep > $OUT/${TAG}_ncu_hw_run.log 2>&1; echo "ncu-hw rc=$?" >> $OUT/${TAG}_ncu_hw_run.log)
   (timeout 900 ncu --set full --clock-control none --import-source on -k regex:adamw_bulk -s 4 -c 1 --target-processes all \
      -o $OUT/${TAG}_adamw python bench.py --steps 1 --warmup 1 --layers 6 --no-e2e --no-streamed \
-     --no-cpu-baseline > $OUT/${TAG}_ncu_full_run.log 2>&1; echo "ncu-full rc=$?" >> $OUT/${TAG}_ncu_full_run.log)
+     --no-cpu-baseline --no-swap-sweep > $OUT/${TAG}_ncu_full_run.log 2>&1; echo "ncu-full rc=$?" >> $OUT/${TAG}_ncu_full_run.log)
 fi
 ls -la $OUT
