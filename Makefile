@@ -21,7 +21,7 @@ CUDA_OBJ := $(patsubst $(PKG)/csrc/cuda/%.cu,$(OBJDIR)/cuda/%.o,$(CUDA_SRC))
 HDRS     := $(wildcard include/offsim/*.hpp include/offsim/*.h include/fuyou/*.h) \
             $(wildcard $(PKG)/csrc/core/*.hpp $(PKG)/csrc/cuda/*.cuh)
 
-all: $(LIBDIR)/liboffsim.so $(if $(CORE_SRC),build/offsim_dump) oracle
+all: $(LIBDIR)/liboffsim.so $(if $(CORE_SRC),build/offsim_dump build/io_engine_test build/offsim) oracle
 
 $(OBJDIR)/core/%.o: $(PKG)/csrc/core/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
@@ -45,6 +45,15 @@ $(LIBDIR)/liboffsim.so: $(LIBDIR)/liboffsim.so.0
 # Parity driver compiled against this repo's headers + core.
 build/offsim_dump: tests/parity/offsim_dump.cpp build/liboffsim_core.a
 	$(CXX) $(CXXFLAGS) $< build/liboffsim_core.a -pthread -o $@
+
+# CLI: links the C ABI only (like the reference's offsim CLI)
+build/offsim: tools/offsim_main.cpp $(LIBDIR)/liboffsim.so
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) $< -L$(LIBDIR) -l:liboffsim.so.0 -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)' -o $@
+
+build/io_engine_test: tests/parity/io_engine_test.cpp $(PKG)/csrc/core/io_engine.cpp $(PKG)/csrc/core/io_engine.hpp
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) tests/parity/io_engine_test.cpp $(PKG)/csrc/core/io_engine.cpp -o $@
 
 oracle:
 	$(MAKE) -C oracle all
