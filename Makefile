@@ -37,7 +37,8 @@ build/liboffsim_core.a: $(CORE_OBJ)
 
 $(LIBDIR)/liboffsim.so.0: $(CORE_OBJ) $(CUDA_OBJ)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -Xlinker -soname=liboffsim.so.0 -o $@ $^ -lpthread
+	$(NVCC) $(ARCH) -shared -Xlinker -soname=liboffsim.so.0 -o $@ $^ -lpthread \
+	    -L/usr/local/cuda/lib64 -lcublas -Xlinker -rpath=/usr/local/cuda/lib64
 
 $(LIBDIR)/liboffsim.so: $(LIBDIR)/liboffsim.so.0
 	ln -sf liboffsim.so.0 $@

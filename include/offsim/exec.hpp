@@ -64,6 +64,11 @@ struct ExecOptions {
     std::string file_dir = "/tmp/offsim_b200";
     bool direct_io = true;          // O_DIRECT for the file tier
     double compute_rate = 0.0;      // FLOP/s of synthetic compute (0: hw.gpu_tput)
+    // fwd/bwd compute tasks: "spin" = timed kernel of work / compute_rate
+    // (no SM/HBM contention); "gemm" = the layer's real bf16 GEMMs through
+    // cuBLAS (fwd: one b*s x out x in GEMM; bwd: dgrad + wgrad), so the
+    // optimizer overlaps real tensor-core work (rate measured, not assumed).
+    std::string compute_mode = "spin";
     std::uint32_t state_slots = 3;  // device staging slots for optimizer groups
     AdamHyper adam;
     std::uint64_t seed = 0;         // synthetic states / grads / activations

@@ -41,7 +41,8 @@ ParsedOptions parse_options(const char* text) {
     static const std::set<std::string> keys = {"device", "tier", "file_dir", "direct_io",
                                                "compute_rate", "state_slots", "seed",
                                                "verify_swaps", "adam", "dry_run", "variant",
-                                               "swap_only", "max_blocks", "placement"};
+                                               "swap_only", "max_blocks", "placement",
+                                               "compute_mode"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -59,6 +60,7 @@ ParsedOptions parse_options(const char* text) {
         o.verify_swaps = doc.value("verify_swaps", o.verify_swaps);
         out.dry_run = doc.value("dry_run", false);
         out.variant = doc.value("variant", std::string());
+        o.compute_mode = doc.value("compute_mode", o.compute_mode);
         o.swap_only = doc.value("swap_only", o.swap_only);
         o.max_blocks = doc.value("max_blocks", o.max_blocks);
         out.placement = doc.value("placement", out.placement);

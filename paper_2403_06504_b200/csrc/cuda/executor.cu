@@ -21,6 +21,7 @@
 #include "offsim/errors.hpp"
 #include "offsim/exec.hpp"
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <fcntl.h>
@@ -218,6 +219,7 @@ public:
         : model_(model), plan_(plan), g_(mapped), opt_(opt), user_(chunks) {}
 
     ~Engine() {
+        if (blas_) cublasDestroy(blas_);
         for (cudaEvent_t e : events_) cudaEventDestroy(e);
         if (base_) cudaEventDestroy(base_);
         for (cudaStream_t s : streams_)
@@ -279,6 +281,17 @@ private:
 
     fy::AdamScalars scalars_{};
     double compute_rate_ = 0.0;
+    // gemm compute mode
+    bool gemm_ = false;
+    cublasHandle_t blas_ = nullptr;
+    Device gemm_a_, gemm_b_, gemm_c_, gemm_ws_;
+    void gemm(cudaStream_t s, int m, int n, int k);
+    void layer_dims(int j, int& in, int& out) const {
+        const int h = static_cast<int>(model_.hidden_dim);
+        static const int kIn[4] = {1, 1, 1, 4}, kOut[4] = {3, 1, 4, 1};
+        in = kIn[j] * h;
+        out = kOut[j] * h;
+    }
 };
 
 std::uint64_t Engine::layer_offset(int j) const {
@@ -395,6 +408,24 @@ void Engine::setup() {
     if (g_.header.variant != ScheduleVariant::overlapped && has_update_)
         for (std::uint32_t k = 0; k < blocks_; ++k) grad_host_.emplace_back(round_up(param_b));
 
+    gemm_ = opt_.compute_mode == "gemm";
+    if (!gemm_ && opt_.compute_mode != "spin")
+        throw ConfigError("executor: compute_mode must be 'spin' or 'gemm'");
+    if (gemm_) {
+        const std::uint64_t tokens = model_.batch_size * model_.seq_len;
+        const std::uint64_t h = model_.hidden_dim;
+        if (tokens > (1ull << 30) || 4 * h > (1ull << 30))
+            throw ConfigError("executor: GEMM dimensions out of range");
+        gemm_a_ = Device(2 * tokens * 4 * h);     // activations  tokens x 4h
+        gemm_b_ = Device(2 * 4 * h * 4 * h);      // weights      4h x 4h (covers 4h x h)
+        gemm_c_ = Device(2 * tokens * 4 * h);     // outputs      tokens x 4h
+        gemm_ws_ = Device(32ull << 20);
+        cudaMemset(gemm_a_.p, 0, 2 * tokens * 4 * h);
+        cudaMemset(gemm_b_.p, 0, 2 * 16 * h * h);
+        if (cublasCreate(&blas_) != CUBLAS_STATUS_SUCCESS) throw fy::DeviceError("cublasCreate failed");
+        cublasSetStream(blas_, lane_stream(ResourceId::gpu_compute));
+        cublasSetWorkspace(blas_, gemm_ws_.p, 32ull << 20);
+    }
     workspace_ = Device(sizeof(float) * fy::kWorkspaceFloats);
     d_norm_ = Device(sizeof(double));
     d_bad_ = Device(sizeof(int));
@@ -524,6 +555,14 @@ MeasuredRates Engine::calibrate() {
         if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
     }
     r.compute_flops = opt_.compute_rate > 0 ? opt_.compute_rate : 0.0;
+    if (gemm_) {
+        // the largest layer GEMM of the model, best of three
+        const int tokens = static_cast<int>(model_.batch_size * model_.seq_len);
+        const int h = static_cast<int>(model_.hidden_dim);
+        const double sec = timed(lane_stream(ResourceId::gpu_compute),
+                                 [&](cudaStream_t s) { gemm(s, tokens, 4 * h, h); });
+        r.compute_flops = 2.0 * tokens * 4.0 * h * h / sec * 1.05;  // upper bound
+    }
     std::size_t free_b = 0, total_b = 0;
     check_cuda(cudaMemGetInfo(&free_b, &total_b), "meminfo");
     r.gpu_mem = total_b;
@@ -532,6 +571,17 @@ MeasuredRates Engine::calibrate() {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     return r;
+}
+
+// C[m x n] = A[m x k] * B[k x n], bf16 in / bf16 out, fp32 accumulate
+// (row-major operands expressed as column-major transposes for cuBLAS).
+void Engine::gemm(cudaStream_t s, int m, int n, int k) {
+    cublasSetStream(blas_, s);
+    const float alpha = 1.0f, beta = 0.0f;
+    const cublasStatus_t st = cublasGemmEx(blas_, CUBLAS_OP_N, CUBLAS_OP_N, n, m, k, &alpha, gemm_b_.p,
+                                           CUDA_R_16BF, n, gemm_a_.p, CUDA_R_16BF, k, &beta, gemm_c_.p,
+                                           CUDA_R_16BF, n, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS) throw fy::DeviceError("cublasGemmEx failed: status " + std::to_string(st));
 }
 
 void Engine::issue(const Task& t, ExecReport& rep) {
@@ -567,6 +617,21 @@ void Engine::issue(const Task& t, ExecReport& rep) {
     const std::string& w = p.what;
     if (t.work <= 0.0) {
         // zero-byte task of the mapped graph (host tier SSD hop, HBM grads)
+    } else if (t.kind == TaskKind::compute && gemm_) {
+        int in = 0, out = 0;
+        layer_dims(j, in, out);
+        const int tokens = static_cast<int>(model_.batch_size * model_.seq_len);
+        if (p.phase == "bwd" && w == "compute") {
+            gemm(s, tokens, in, out);  // dgrad: dY[t x out] * W^T -> dX[t x in]
+            gemm(s, in, out, tokens);  // wgrad: X^T[in x t] * dY -> dW[in x out]
+        } else {
+            gemm(s, tokens, out, in);  // forward / recompute
+        }
+        // attention-score extras (extra_flops_per_block) stay timed
+        const double extra = t.work - (p.phase == "bwd" && w == "compute" ? 4.0 : 2.0) *
+                                          double(tokens) * in * out;
+        if (extra > 1.0) spin_kernel<<<1, 32, 0, s>>>(static_cast<std::uint64_t>(extra / compute_rate_ * 1e9));
+        check_cuda(cudaGetLastError(), "compute launch");
     } else if (t.kind == TaskKind::compute) {
         const double sec = t.work / compute_rate_;
         spin_kernel<<<1, 32, 0, s>>>(static_cast<std::uint64_t>(sec * 1e9));

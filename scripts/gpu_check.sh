@@ -17,16 +17,13 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   (timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'adamw|reduce_partials|grad_stats' -c 400 --csv \
      --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e \
      --no-streamed --no-cpu-baseline --no-swap-sweep > $OUT/${TAG}_ncu_launch_run.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/${TAG}_ncu_launch_run.log)
-  # hardware-counter sections only: the SASS-patching sections (SourceCounters,
-  # InstructionStats) instrument the TMA kernel's mbarrier spin-waits and
-  # inflate both its duration and its DRAM traffic
-  (timeout 900 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section MemoryWorkloadAnalysis_Tables \
-     --section LaunchStats --section Occupancy --section SchedulerStats --section WarpStateStats \
-     --section ComputeWorkloadAnalysis --clock-control none -k regex:adamw_bulk -s 4 -c 1 \
-     -o $OUT/${TAG}_adamw_hw python bench.py --steps 1 --warmup 1 --layers 6 --no-e2e --no-streamed \
-     --no-cpu-baseline --no-swap-sweep > $OUT/${TAG}_ncu_hw_run.log 2>&1; echo "ncu-hw rc=$?" >> $OUT/${TAG}_ncu_hw_run.log)
-  (timeout 900 ncu --set full --clock-control none --import-source on -k regex:adamw_bulk -s 4 -c 1 --target-processes all \
-     -o $OUT/${TAG}_adamw python bench.py --steps 1 --warmup 1 --layers 6 --no-e2e --no-streamed \
-     --no-cpu-baseline --no-swap-sweep > $OUT/${TAG}_ncu_full_run.log 2>&1; echo "ncu-full rc=$?" >> $OUT/${TAG}_ncu_full_run.log)
+  # single-pass DRAM traffic of the fused kernel (no replay)
+  (timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+     --clock-control none -k regex:adamw_ -c 6 --csv --log-file $OUT/${TAG}_traffic.csv \
+     python scripts/ncu_target.py > $OUT/${TAG}_ncu_traffic_run.log 2>&1; echo "ncu-traffic rc=$?" >> $OUT/${TAG}_ncu_traffic_run.log)
+  # full section set; application replay (kernel replay perturbs the TMA kernel)
+  (timeout 1200 ncu --set full --replay-mode application --clock-control none --import-source on \
+     -k regex:adamw_ -s 2 -c 1 -o $OUT/${TAG}_adamw python scripts/ncu_target.py \
+     > $OUT/${TAG}_ncu_full_run.log 2>&1; echo "ncu-full rc=$?" >> $OUT/${TAG}_ncu_full_run.log)
 fi
 ls -la $OUT

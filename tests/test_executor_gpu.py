@@ -123,3 +123,14 @@ def test_serial_file_tier(cuda_dev, tmp_path):
         if name != "makespan-equals-duration-sum":
             assert ok, (name, detail)
     assert inv["strictly-serial"][0]
+
+
+def test_c1_gemm_compute_mode_matches_oracle(cuda_dev):
+    # fwd/bwd compute as real cuBLAS bf16 GEMMs: the optimizer overlaps
+    # tensor-core work; the Adam results must not change by a bit
+    chunks, ref = _chunks(cuda_dev, seed=300)
+    st, s, err = graph_execute(scenario(), {"tier": "host", "compute_mode": "gemm"}, chunks)
+    assert st == 0, (err, _failing(s))
+    assert s["all_invariants_pass"], s["invariants"]
+    assert s["hw_exec"]["gpu_tput"] > 1e14  # measured GEMM rate, not the preset's
+    _oracle_check(chunks, ref, s)
