@@ -34,7 +34,6 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
-#include <numeric>
 #include <sstream>
 
 namespace offsim {
@@ -152,8 +151,6 @@ private:
 };
 
 // ------------------------------------------------------------- parsing
-
-enum class Op { noop, h2d, d2h, file_read, file_write, compute, update };
 
 struct Parsed {
     std::string phase, what; // "fwd","p_c2g"
@@ -416,12 +413,16 @@ void Engine::setup() {
         const std::uint64_t h = model_.hidden_dim;
         if (tokens > (1ull << 30) || 4 * h > (1ull << 30))
             throw ConfigError("executor: GEMM dimensions out of range");
-        gemm_a_ = Device(2 * tokens * 4 * h);     // activations  tokens x 4h
-        gemm_b_ = Device(2 * 4 * h * 4 * h);      // weights      4h x 4h (covers 4h x h)
-        gemm_c_ = Device(2 * tokens * 4 * h);     // outputs      tokens x 4h
+        // operand extents over fwd (t x in x out), dgrad (t x out -> in) and
+        // wgrad (in x t x out): A <= t*4h, B <= max(4h^2, t*4h), C <= max(t*4h, 4h^2)
+        const std::uint64_t a_elems = tokens * 4 * h;
+        const std::uint64_t bc_elems = std::max(4 * h * h, tokens * 4 * h);
+        gemm_a_ = Device(2 * a_elems);
+        gemm_b_ = Device(2 * bc_elems);
+        gemm_c_ = Device(2 * bc_elems);
         gemm_ws_ = Device(32ull << 20);
-        cudaMemset(gemm_a_.p, 0, 2 * tokens * 4 * h);
-        cudaMemset(gemm_b_.p, 0, 2 * 16 * h * h);
+        check_cuda(cudaMemset(gemm_a_.p, 0, 2 * a_elems), "memset");
+        check_cuda(cudaMemset(gemm_b_.p, 0, 2 * bc_elems), "memset");
         if (cublasCreate(&blas_) != CUBLAS_STATUS_SUCCESS) throw fy::DeviceError("cublasCreate failed");
         cublasSetStream(blas_, lane_stream(ResourceId::gpu_compute));
         cublasSetWorkspace(blas_, gemm_ws_.p, 32ull << 20);
@@ -716,10 +717,8 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
     check_cuda(cudaDeviceSynchronize(), "pre-run sync");
     check_cuda(cudaEventRecord(base_, streams_[0]), "base");
     for (int r = 1; r < 5; ++r) check_cuda(cudaStreamWaitEvent(streams_[r], base_, 0), "base wait");
-    const auto wall0 = std::chrono::steady_clock::now();
     for (const auto& [start, id] : order) issue(g_.tasks[id], rep);
     check_cuda(cudaDeviceSynchronize(), "executor run");
-    (void)wall0;
     if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
 
     // swap integrity: every restored buffer equals its original
