@@ -78,6 +78,7 @@ def parse():
     ap.add_argument("--streamed-pieces", type=int, default=4)
     ap.add_argument("--cpu-sample-chunks", type=int, default=2)
     ap.add_argument("--no-swap-sweep", action="store_true")
+    ap.add_argument("--no-backward-overlap", action="store_true")
     ap.add_argument("--layers", type=int, default=C2["layers"], help="override (debug only)")
     ap.add_argument("--hidden", type=int, default=C2["hidden"], help="override (debug only)")
     return ap.parse_args()
@@ -316,6 +317,9 @@ def streamed_phase(torch, F, args, pcie):
         pipe.wait()
     el = (time.perf_counter() - t0) / reps
     tim, step_ns = pipe.timings(K * P)
+    overlap = None
+    if not args.no_backward_overlap:
+        overlap = streamed_backward_overlap(torch, pipe, chunks, hp, K, P, el)
     d2h_busy = sum(t["d2h"][1] - t["d2h"][0] for t in tim) * 1e-9
     h2d_busy = sum(t["h2d"][1] - t["h2d"][0] for t in tim) * 1e-9
     rate = K * N / el
@@ -332,12 +336,72 @@ def streamed_phase(torch, F, args, pcie):
                      "frac": d2h_gbs / pcie["duplex_each_gbs"],
                      "peak_source": "in-run pinned cudaMemcpyAsync, H2D+D2H concurrent (1 GiB)"},
     }
+    if overlap is not None:
+        overlap["with_backward_d2h_frac"] = 14 * N * K / overlap["step_s"] / 1e9 / pcie["duplex_each_gbs"]
+        out["with_backward"] = overlap
     pipe.close()
     del grads
     for p in ptrs:
         F.check(F.LIB.fy_host_free(p))
     torch.cuda.empty_cache()
     return out
+
+
+def streamed_backward_overlap(torch, pipe, chunks, hp, K, P, t_stream):
+    """The streamed step overlapped with a synthetic backward (SURVEY.md §8
+    C3): real bf16 GEMMs of the 65B block (b=16, s=1024, h=8192; per block
+    the recompute forward 24*t*h^2 plus dgrad + wgrad 48*t*h^2 FLOPs, t =
+    b*s tokens) on a separate stream, in the optimizer's block order; every
+    piece of block k waits (fy_chunk.grad_ready) on the event recorded after
+    block k's backward. Reports the step time with backward running, the
+    backward alone, and the overlap efficiency
+    (t_stream + t_bwd - t_both) / min(t_stream, t_bwd): 1.0 = fully hidden."""
+    h, t = C3["hidden"], 16 * 1024
+    dev = torch.device("cuda")
+    dims = [(h, 3 * h), (h, h), (h, 4 * h), (4 * h, h)]  # (in, out) of the block's linears
+    X = [torch.randn(t, i, device=dev, dtype=torch.bfloat16) for i, _ in dims]
+    Y = [torch.randn(t, o, device=dev, dtype=torch.bfloat16) for _, o in dims]
+    W = [torch.randn(i, o, device=dev, dtype=torch.bfloat16) * 0.01 for i, o in dims]
+    G = [torch.empty(i, o, device=dev, dtype=torch.bfloat16) for i, o in dims]
+    bwd = torch.cuda.Stream(dev, priority=0)
+
+    def block_backward():
+        for j in range(4):                     # recompute forward
+            torch.matmul(X[j], W[j], out=Y[j])
+        for j in reversed(range(4)):
+            torch.matmul(Y[j], W[j].t(), out=X[j])   # dgrad
+            torch.matmul(X[j].t(), Y[j], out=G[j])   # wgrad
+
+    def run_backward(events=None):
+        with torch.cuda.stream(bwd):
+            for k in range(K):
+                block_backward()
+                if events is not None:
+                    events[k].record(bwd)
+
+    run_backward()  # warm cuBLAS
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run_backward()
+    torch.cuda.synchronize()
+    t_bwd = time.perf_counter() - t0
+    flops = K * 72 * t * h * h
+    ev = [torch.cuda.Event() for _ in range(K)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run_backward(ev)  # records the events (created on first record)
+    gated = [dict(c, grad_ready=ev[i // P].cuda_event) for i, c in enumerate(chunks)]
+    pipe.step(gated, hp)
+    pipe.wait()
+    torch.cuda.synchronize()
+    t_both = time.perf_counter() - t0
+    del X, Y, W, G
+    return {"step_s": t_both, "stream_alone_s": t_stream, "backward_alone_s": t_bwd,
+            "backward_tflops_alone": flops / t_bwd / 1e12,
+            "overlap_efficiency": (t_stream + t_bwd - t_both) / min(t_stream, t_bwd),
+            "value": K * C3["chunk"] / t_both, "unit": UNIT,
+            "backward": "bf16 cuBLAS GEMMs (torch.matmul) of the 65B block, b=16 s=1024, "
+                        "72*t*h^2 FLOPs/block, separate stream"}
 
 
 def resident_phase(torch, F, args, world, rank, local):

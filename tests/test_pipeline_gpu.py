@@ -89,3 +89,39 @@ def test_pipeline_rejects_bad_args(cuda_dev):
     pipe.close()
     with pytest.raises(FyError):
         F.ChunkPipeline(1024, slots=1)
+
+
+def test_pipeline_waits_for_grad_ready_events(cuda_dev):
+    """Each chunk's update must wait on its producer's event (the backward
+    that writes the grads): the grads are written late on a
+    side stream (after a ~50 ms spin); reading them early would use zeros."""
+    from paper_2403_06504_b200 import optim as F
+    sizes = [1 << 20, (1 << 20) + 5, 65536]
+    chunks, ref = _make_chunks(sizes, 7, cuda_dev, grads_on_host=False)
+    late = [c["grad_t"].clone() for c in chunks]
+    for c in chunks:
+        c["grad_t"].zero_()
+    side = torch.cuda.Stream()
+    evs = []
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        for c, g in zip(chunks, late):
+            torch.cuda._sleep(50_000_000)
+            c["grad_t"].copy_(g)
+            e = torch.cuda.Event()
+            e.record(side)
+            evs.append(e)
+    desc = _desc(chunks)
+    for d, e in zip(desc, evs):
+        d["grad_ready"] = e.cuda_event
+    pipe = F.ChunkPipeline(max(sizes), slots=2)
+    pipe.step(desc, F.Hparams(step=10))
+    pipe.wait()
+    sc = O.scalars(step=10)
+    for c, r in zip(chunks, ref):
+        n = r["grad"].size
+        st = r["states"]
+        mst, mm, vv = st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()
+        O.adamw_step(mst, mm, vv, r["grad"], O.BF16, sc)
+        assert _bits_equal(c["h_states_t"].numpy(), np.concatenate([mst, mm, vv]))
+    pipe.close()
