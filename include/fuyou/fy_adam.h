@@ -112,7 +112,9 @@ fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad
  * path 0: LSU kernel, `unroll` quads (4 elements) per thread per grid-stride
  *         iteration in {1,2,4,8}, `ctas_per_sm` resident CTAs (0 = occupancy);
  * path 1: TMA bulk-copy kernel (cp.async.bulk + mbarrier), `unroll` = stages
- *         in {2,3,4,6}. Default: path 1, 3 stages (measured best, profiles/). */
+ *         in {2,3,4,6}, third argument = consumer warps per CTA (4 or 8;
+ *         0 = 8; 6 stages only with 8). Default: path 1, 3 stages, 8 warps
+ *         (measured best, profiles/). */
 fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
 
 /* Number of SMs and the launch geometry the kernels use on `device`

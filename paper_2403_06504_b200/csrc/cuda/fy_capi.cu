@@ -205,6 +205,8 @@ extern "C" fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm) {
     if (path == 1 && (unroll < 2 || unroll > 6 || unroll == 5))
         return fail(FY_ERR_CONFIG, "stages must be 2, 3, 4 or 6");
     if (ctas_per_sm < 0 || ctas_per_sm > 32) return fail(FY_ERR_CONFIG, "ctas_per_sm out of range");
+    if (path == 1 && ctas_per_sm != 0 && ctas_per_sm != 4 && ctas_per_sm != 8)
+        return fail(FY_ERR_CONFIG, "path 1: third argument is the consumer warp count (4 or 8)");
     fy::set_tuning(path, unroll, ctas_per_sm);
     return FY_OK;
 }
