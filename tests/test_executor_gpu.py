@@ -134,3 +134,24 @@ def test_c1_gemm_compute_mode_matches_oracle(cuda_dev):
     assert s["all_invariants_pass"], s["invariants"]
     assert s["hw_exec"]["gpu_tput"] > 1e14  # measured GEMM rate, not the preset's
     _oracle_check(chunks, ref, s)
+
+
+@pytest.mark.parametrize("placement,tier", [("auto", "host"), ("ssd", "file")])
+def test_swap_only_subgraph(cuda_dev, tmp_path, placement, tier):
+    # BASELINE config 5 path: only the activation-swap tasks, first 3 blocks
+    # of C1 at b=128. The planner swaps 13 layers: the 12 linear_4htoh
+    # (priority queue) + block 0's linear_qkv -> 4 activations + 3
+    # checkpoints in blocks 0-2
+    opts = {"tier": tier, "swap_only": True, "max_blocks": 3, "placement": placement,
+            "file_dir": str(tmp_path)}
+    st, s, _, err = execute(scenario(batch=128), opts)
+    assert st == 0, (err, _failing(s))
+    assert s["all_invariants_pass"], s["invariants"]
+    assert s["swap_checks"] == 4 + 3 and s["swap_mismatches"] == 0
+    rb, pb = s["reference_bytes"], s["physical_bytes"]
+    assert pb["d2h/activations"] == rb["link_g2c/activations"]
+    assert pb["h2d/activations"] == rb["link_c2g/activations"]
+    if placement == "ssd":
+        assert s["io_engine"] in ("io_uring", "pread/pwrite")
+        assert pb["file_write/activations"] + pb["file_read/activations"] == rb["link_ssd/activations"]
+    assert "h2d/opt_states" not in pb  # no optimizer state touched
