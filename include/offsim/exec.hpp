@@ -78,6 +78,14 @@ struct ExecOptions {
     // (0 = all blocks).
     bool swap_only = false;
     std::uint32_t max_blocks = 0;
+    // File tier with bounded pinned staging (the SSD tier proper): 0 keeps a
+    // host copy of every chunk; N > 0 stages optimizer states, params and
+    // weights through N-slot pinned rings (and activations too when the
+    // plan places them on SSD), so host memory no longer scales with the
+    // model. Ring reuse is expressed as graph edges (add_host_ring_edges).
+    std::uint32_t host_ring = 0;
+    // Report an FNV-1a checksum of every chunk's final [master|m|v].
+    bool checksum_states = false;
 };
 
 // Caller-provided optimizer states for chunk (block) k: pinned host
@@ -95,6 +103,13 @@ struct ChunkBuffers {
 // slot m % state_slots; the slot-reuse edge is part of the mapped graph.
 TaskGraph map_graph_for_b200(const TaskGraph& graph, StateTier tier,
                              std::uint32_t state_slots = 3);
+
+// Slot-reuse edges of the bounded host staging rings (file tier): the n-th
+// use of a ring waits for the last task of use n - slots. Uses are, in task
+// id order: optimizer groups (state_s2c .. state_c2s), param write-backs
+// (param_d2h .. param_c2s), weight fetches (p_s2c .. p_c2g) and, when
+// checkpoints live on SSD, activation transfers (g2c .. c2s, s2c .. c2g).
+void add_host_ring_edges(TaskGraph& mapped, std::uint32_t slots);
 
 // The activation-swap path of a (mapped) graph: every task with payload
 // activations whose block index is < max_blocks (0 = all), dependencies
@@ -129,6 +144,8 @@ struct ExecReport {
     std::uint64_t swap_mismatches = 0; // must be 0
     std::uint32_t kernel_launches = 0;
     std::string io_engine; // "io_uring" | "pread/pwrite" (file tier)
+    std::uint64_t pinned_host_bytes = 0;  // host staging the run allocated
+    std::uint64_t state_checksum = 0;     // checksum_states
 };
 
 ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const SwapPlan& plan,

@@ -42,7 +42,7 @@ ParsedOptions parse_options(const char* text) {
                                                "compute_rate", "state_slots", "seed",
                                                "verify_swaps", "adam", "dry_run", "variant",
                                                "swap_only", "max_blocks", "placement",
-                                               "compute_mode"};
+                                               "compute_mode", "host_ring", "checksum_states"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -61,6 +61,8 @@ ParsedOptions parse_options(const char* text) {
         out.dry_run = doc.value("dry_run", false);
         out.variant = doc.value("variant", std::string());
         o.compute_mode = doc.value("compute_mode", o.compute_mode);
+        o.host_ring = doc.value("host_ring", o.host_ring);
+        o.checksum_states = doc.value("checksum_states", o.checksum_states);
         o.swap_only = doc.value("swap_only", o.swap_only);
         o.max_blocks = doc.value("max_blocks", o.max_blocks);
         out.placement = doc.value("placement", out.placement);
@@ -156,6 +158,8 @@ std::string exec_summary_json(const ExecReport& r) {
         {"swap_mismatches", r.swap_mismatches},
         {"kernel_launches", r.kernel_launches},
         {"io_engine", r.io_engine},
+        {"pinned_host_bytes", r.pinned_host_bytes},
+        {"state_checksum", r.state_checksum},
         {"invariants", checks},
         {"all_invariants_pass", r.invariants.all_pass && r.swap_mismatches == 0},
     };
@@ -183,6 +187,7 @@ std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVar
     const TaskGraph ref = build_schedule(s.model, s.hardware, plan, v);
     TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots);
     if (po.exec.swap_only) mapped = swap_subgraph(mapped, po.exec.max_blocks);
+    if (po.exec.tier == StateTier::file && po.exec.host_ring > 0) add_host_ring_edges(mapped, po.exec.host_ring);
     MeasuredRates nominal;
     nominal.h2d_bps = nominal.d2h_bps = 55e9;
     nominal.file_read_bps = nominal.file_write_bps = po.exec.tier == StateTier::file ? 2e9 : 0.0;

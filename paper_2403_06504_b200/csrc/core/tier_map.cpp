@@ -153,6 +153,44 @@ TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t 
     return out;
 }
 
+void add_host_ring_edges(TaskGraph& g, std::uint32_t slots) {
+    if (slots == 0) return;
+    std::map<std::string, std::uint32_t> by_name;
+    for (const Task& t : g.tasks) by_name[t.name] = t.id;
+    struct Use {
+        std::uint32_t first, last;
+    };
+    std::vector<Use> states, params, weights, acts;
+    const bool acts_on_ssd = g.header.checkpoint_location == "ssd";
+    auto partner = [&](const std::string& name, const char* from, const char* to) {
+        std::string other = name;
+        other.replace(other.find(from), std::strlen(from), to);
+        const auto it = by_name.find(other);
+        return it == by_name.end() ? 0xffffffffu : it->second;
+    };
+    for (const Task& t : g.tasks) {
+        const std::string& n = t.name;
+        if (starts_with(n, "opt state_s2c ")) states.push_back({t.id, partner(n, "state_s2c", "state_c2s")});
+        else if (starts_with(n, "opt param_d2h ")) params.push_back({t.id, partner(n, "param_d2h", "param_c2s")});
+        else if (n.find(" p_s2c ") != std::string::npos) weights.push_back({t.id, partner(n, "p_s2c", "p_c2g")});
+        else if (acts_on_ssd && (starts_with(n, "fwd act_g2c ") || starts_with(n, "fwd ckpt_g2c ")))
+            acts.push_back({t.id, partner(n, "_g2c", "_c2s")});
+        else if (acts_on_ssd && (starts_with(n, "bwd act_s2c ") || starts_with(n, "bwd ckpt_s2c ")))
+            acts.push_back({t.id, partner(n, "_s2c", "_c2g")});
+    }
+    for (std::vector<Use>* uses : {&states, &params, &weights, &acts}) {
+        for (std::size_t k = slots; k < uses->size(); ++k) {
+            const Use& prev = (*uses)[k - slots];
+            if (prev.last == 0xffffffffu) throw InvariantError("host ring: unpaired task '" + g.tasks[prev.first].name + "'");
+            Task& t = g.tasks[(*uses)[k].first];
+            if (prev.last >= t.id) throw InvariantError("host ring edge would not be topological at '" + t.name + "'");
+            t.deps.push_back(prev.last);
+            std::sort(t.deps.begin(), t.deps.end());
+            t.deps.erase(std::unique(t.deps.begin(), t.deps.end()), t.deps.end());
+        }
+    }
+}
+
 TaskGraph swap_subgraph(const TaskGraph& in, std::uint32_t max_blocks) {
     TaskGraph out;
     out.header = in.header;

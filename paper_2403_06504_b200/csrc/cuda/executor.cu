@@ -247,6 +247,31 @@ private:
     bool file_tier_ = false;
     bool has_update_ = false;
     bool has_weights_ = false;
+    // bounded pinned staging rings (file tier, host_ring > 0)
+    bool ring_ = false;
+    bool acts_on_ssd_ = false;
+    std::vector<Pinned> state_ring_, param_ring_, weight_ring_, act_ring_;
+    std::map<std::uint32_t, int> ring_slot_; // task id -> ring slot
+    std::uint64_t pinned_bytes_ = 0;
+    Pinned pin(std::uint64_t bytes) {
+        pinned_bytes_ += std::max<std::uint64_t>(bytes, kAlign);
+        return Pinned(bytes);
+    }
+    void* ring_ptr(std::vector<Pinned>& r, std::uint32_t task) { return r[ring_slot_.at(task)].p; }
+    void* host_states(std::uint32_t task, std::uint32_t k) {
+        return ring_ ? ring_ptr(state_ring_, task) : h_states_[k];
+    }
+    void* host_params(std::uint32_t task, std::uint32_t k) {
+        return ring_ ? ring_ptr(param_ring_, task) : h_params_[k];
+    }
+    void* host_weights(std::uint32_t task, std::uint32_t k, std::uint64_t layer_off) {
+        return ring_ ? ring_ptr(weight_ring_, task) : static_cast<char*>(h_params_[k]) + layer_off;
+    }
+    void* host_act(std::uint32_t task, const Pinned& unit) {
+        return ring_ && acts_on_ssd_ ? ring_ptr(act_ring_, task) : unit.p;
+    }
+    std::uint64_t checksum_states();
+    void assign_ring_slots();
 
     cudaStream_t streams_[5] = {};
     std::vector<cudaEvent_t> events_;
@@ -336,6 +361,9 @@ void Engine::setup() {
         if (p.what.rfind("ckpt_", 0) == 0) ckpt_used[p.block] = true;
     }
     const bool need_chunks = has_update_ || has_weights_;
+    ring_ = file_tier_ && opt_.host_ring > 0;
+    acts_on_ssd_ = g_.header.checkpoint_location == "ssd";
+    if (ring_ && user_) throw ConfigError("executor: host_ring stages synthetic states only (offsim_execute)");
     h_states_.assign(blocks_, nullptr);
     h_params_.assign(blocks_, nullptr);
     d_grads_.assign(blocks_, nullptr);
@@ -343,9 +371,9 @@ void Engine::setup() {
         if (user_ && (*user_)[k].host_states) {
             h_states_[k] = (*user_)[k].host_states;
             h_params_[k] = (*user_)[k].host_params;
-        } else {
-            own_states_.emplace_back(round_up(state_b));
-            own_params_.emplace_back(round_up(param_b));
+        } else if (!ring_) {
+            own_states_.push_back(pin(round_up(state_b)));
+            own_params_.push_back(pin(round_up(param_b)));
             h_states_[k] = own_states_.back().p;
             h_params_[k] = own_params_.back().p;
         }
@@ -358,7 +386,7 @@ void Engine::setup() {
         }
     }
     // synthetic host states when not provided: generate on the device, copy
-    if (need_chunks && !(user_ && (*user_)[0].host_states)) {
+    if (need_chunks && !ring_ && !(user_ && (*user_)[0].host_states)) {
         Device tmp(state_b);
         for (std::uint32_t k = 0; k < blocks_; ++k) {
             fill_states<<<592, 256>>>(static_cast<float*>(tmp.p), n_, seed + 7 * k);
@@ -387,7 +415,7 @@ void Engine::setup() {
         const std::uint64_t b = round_up(layers_[i].act_bytes);
         act_dev_[i] = Device(b);
         act_restore_[i] = Device(b);
-        act_host_[i] = Pinned(b);
+        if (!(ring_ && acts_on_ssd_)) act_host_[i] = pin(b);
         fill_pattern<<<296, 256>>>(static_cast<std::uint64_t*>(act_dev_[i].p), b / 8, seed ^ (i + 1));
     }
     ckpt_dev_.resize(blocks_);
@@ -398,12 +426,30 @@ void Engine::setup() {
         const std::uint64_t b = round_up(ckpt_bytes_);
         ckpt_dev_[k] = Device(b);
         ckpt_restore_[k] = Device(b);
-        ckpt_host_[k] = Pinned(b);
+        if (!(ring_ && acts_on_ssd_)) ckpt_host_[k] = pin(b);
         fill_pattern<<<296, 256>>>(static_cast<std::uint64_t*>(ckpt_dev_[k].p), b / 8,
                                    seed ^ (0xc0ffee00ull + k));
     }
     if (g_.header.variant != ScheduleVariant::overlapped && has_update_)
-        for (std::uint32_t k = 0; k < blocks_; ++k) grad_host_.emplace_back(round_up(param_b));
+        for (std::uint32_t k = 0; k < blocks_; ++k) grad_host_.push_back(pin(round_up(param_b)));
+
+    if (ring_) {
+        const std::uint32_t R = opt_.host_ring;
+        std::uint64_t max_w = 0, max_act = ckpt_bytes_;
+        for (std::size_t i = 0; i < layers_.size(); ++i) {
+            max_w = std::max(max_w, layers_[i].param_bytes);
+            if (swapped_[i]) max_act = std::max(max_act, layers_[i].act_bytes);
+        }
+        for (std::uint32_t r = 0; r < R; ++r) {
+            if (has_update_) {
+                state_ring_.push_back(pin(round_up(state_b)));
+                param_ring_.push_back(pin(round_up(param_b)));
+            }
+            if (has_weights_) weight_ring_.push_back(pin(round_up(max_w)));
+            if (acts_on_ssd_) act_ring_.push_back(pin(round_up(max_act)));
+        }
+        assign_ring_slots();
+    }
 
     gemm_ = opt_.compute_mode == "gemm";
     if (!gemm_ && opt_.compute_mode != "spin")
@@ -459,11 +505,27 @@ void Engine::setup() {
         if (!grad_host_.empty())
             f_grads_ = std::make_unique<TierFile>(stem + "grads.bin", blocks_ * round_up(param_b), direct);
         // the tier holds the initial states / params before the step
+        std::unique_ptr<Device> gen;
+        Pinned stage_s, stage_p;
+        if (ring_ && chunks) {
+            gen = std::make_unique<Device>(state_b);
+            stage_s = Pinned(round_up(state_b));
+            stage_p = Pinned(round_up(param_b));
+            std::memset(stage_p.p, 0, round_up(param_b));
+        }
         for (std::uint32_t k = 0; k < blocks_ && chunks; ++k) {
-            IoRequest w{&io_, f_states_->fd(), h_states_[k], round_up(state_b), k * round_up(state_b), true,
+            void* src_s = h_states_[k];
+            void* src_p = h_params_[k];
+            if (ring_) { // generate chunk k on the device, stage it, write it
+                fill_states<<<592, 256>>>(static_cast<float*>(gen->p), n_, seed + 7 * k);
+                check_cuda(cudaMemcpy(stage_s.p, gen->p, state_b, cudaMemcpyDeviceToHost), "seed states");
+                src_s = stage_s.p;
+                src_p = stage_p.p;
+            }
+            IoRequest w{&io_, f_states_->fd(), src_s, round_up(state_b), k * round_up(state_b), true,
                         false, &io_error_, &io_error_text_, &io_mu_};
             run_io(&w);
-            IoRequest wp{&io_, f_params_->fd(), h_params_[k], round_up(param_b), k * round_up(param_b), true,
+            IoRequest wp{&io_, f_params_->fd(), src_p, round_up(param_b), k * round_up(param_b), true,
                          false, &io_error_, &io_error_text_, &io_mu_};
             run_io(&wp);
         }
@@ -574,6 +636,71 @@ MeasuredRates Engine::calibrate() {
     return r;
 }
 
+// Ring slot of every task that touches a staging ring; same use order as
+// add_host_ring_edges (task id order), so the graph's reuse edges protect
+// exactly these slots.
+void Engine::assign_ring_slots() {
+    std::map<std::string, std::uint32_t> id_of;
+    for (const Task& t : g_.tasks) id_of[t.name] = t.id;
+    const std::uint32_t R = opt_.host_ring;
+    std::uint32_t ns = 0, np = 0, nw = 0, na = 0;
+    auto tie = [&](const std::string& name, int slot) {
+        const auto it = id_of.find(name);
+        if (it != id_of.end()) ring_slot_[it->second] = slot;
+    };
+    auto swap_name = [](std::string n, const char* a, const char* b) {
+        n.replace(n.find(a), std::strlen(a), b);
+        return n;
+    };
+    for (const Task& t : g_.tasks) {
+        const std::string& n = t.name;
+        if (n.rfind("opt state_s2c ", 0) == 0) {
+            const int slot = static_cast<int>(ns++ % R);
+            for (const char* w : {"state_s2c", "state_h2d", "state_d2h", "state_c2s"})
+                tie(swap_name(n, "state_s2c", w), slot);
+        } else if (n.rfind("opt param_d2h ", 0) == 0) {
+            const int slot = static_cast<int>(np++ % R);
+            tie(n, slot);
+            tie(swap_name(n, "param_d2h", "param_c2s"), slot);
+        } else if (n.find(" p_s2c ") != std::string::npos) {
+            const int slot = static_cast<int>(nw++ % R);
+            tie(n, slot);
+            tie(swap_name(n, "p_s2c", "p_c2g"), slot);
+        } else if (acts_on_ssd_ && (n.rfind("fwd act_g2c ", 0) == 0 || n.rfind("fwd ckpt_g2c ", 0) == 0)) {
+            const int slot = static_cast<int>(na++ % R);
+            tie(n, slot);
+            tie(swap_name(n, "_g2c", "_c2s"), slot);
+        } else if (acts_on_ssd_ && (n.rfind("bwd act_s2c ", 0) == 0 || n.rfind("bwd ckpt_s2c ", 0) == 0)) {
+            const int slot = static_cast<int>(na++ % R);
+            tie(n, slot);
+            tie(swap_name(n, "_s2c", "_c2g"), slot);
+        }
+    }
+}
+
+// FNV-1a over 64-bit words of every chunk's final [master|m|v], read back
+// from the file tier (or the pinned host copies) after the run.
+std::uint64_t Engine::checksum_states() {
+    const std::uint64_t state_b = 12 * n_;
+    std::uint64_t h = 1469598103934665603ull;
+    Pinned tmp;
+    if (file_tier_) tmp = Pinned(round_up(state_b));
+    for (std::uint32_t k = 0; k < blocks_; ++k) {
+        const void* src = h_states_[k];
+        if (file_tier_) {
+            IoRequest r{&io_, f_states_->fd(), tmp.p, round_up(state_b), k * round_up(state_b), false, false,
+                        &io_error_, &io_error_text_, &io_mu_};
+            run_io(&r);
+            src = tmp.p;
+        }
+        if (!src) continue;
+        const auto* w = static_cast<const std::uint64_t*>(src);
+        for (std::uint64_t i = 0; i < state_b / 8; ++i) h = (h ^ w[i]) * 1099511628211ull;
+    }
+    if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
+    return h;
+}
+
 // C[m x n] = A[m x k] * B[k x n], bf16 in / bf16 out, fp32 accumulate
 // (row-major operands expressed as column-major transposes for cuBLAS).
 void Engine::gemm(cudaStream_t s, int m, int n, int k) {
@@ -658,40 +785,41 @@ void Engine::issue(const Task& t, ExecReport& rep) {
         rep.kernel_launches += 2;
     } else if (w == "state_h2d") {
         // the slot's previous user (state_d2h of group m - slots) is a dep
-        h2d(slots_[slot_of(k)].p, h_states_[k], state_b);
+        h2d(slots_[slot_of(k)].p, host_states(t.id, k), state_b);
     } else if (w == "state_d2h") {
-        d2h(h_states_[k], slots_[slot_of(k)].p, state_b);
+        d2h(host_states(t.id, k), slots_[slot_of(k)].p, state_b);
     } else if (w == "param_d2h") {
-        d2h(h_params_[k], d_grads_[k], param_b);
+        d2h(host_params(t.id, k), d_grads_[k], param_b);
     } else if (w == "state_s2c") {
-        file(*f_states_, h_states_[k], state_b, k * round_up(state_b), false, false);
+        file(*f_states_, host_states(t.id, k), state_b, k * round_up(state_b), false, false);
     } else if (w == "state_c2s") {
-        file(*f_states_, h_states_[k], state_b, k * round_up(state_b), true, false);
+        file(*f_states_, host_states(t.id, k), state_b, k * round_up(state_b), true, false);
     } else if (w == "param_c2s") {
-        file(*f_params_, h_params_[k], param_b, k * round_up(param_b), true, false);
+        file(*f_params_, host_params(t.id, k), param_b, k * round_up(param_b), true, false);
     } else if (w == "p_s2c") {
         const std::uint64_t off = layer_offset(j);
-        file(*f_params_, static_cast<char*>(h_params_[k]) + off, layers_[li].param_bytes,
+        file(*f_params_, host_weights(t.id, k, off), layers_[li].param_bytes,
              k * round_up(param_b) + off, false, false);
     } else if (w == "p_c2g") {
         void* dst = wscratch_[wscratch_turn_ ^= 1].p;
-        h2d(dst, static_cast<char*>(h_params_[k]) + layer_offset(j), layers_[li].param_bytes);
+        h2d(dst, host_weights(t.id, k, layer_offset(j)), layers_[li].param_bytes);
     } else if (w == "act_g2c") {
-        d2h(act_host_[li].p, act_dev_[li].p, layers_[li].act_bytes);
+        d2h(host_act(t.id, act_host_[li]), act_dev_[li].p, layers_[li].act_bytes);
     } else if (w == "act_c2s") {
-        file(*f_acts_, act_host_[li].p, layers_[li].act_bytes, act_file_off_[li], true, opt_.verify_swaps);
+        file(*f_acts_, host_act(t.id, act_host_[li]), layers_[li].act_bytes, act_file_off_[li], true,
+             opt_.verify_swaps);
     } else if (w == "act_s2c") {
-        file(*f_acts_, act_host_[li].p, layers_[li].act_bytes, act_file_off_[li], false, false);
+        file(*f_acts_, host_act(t.id, act_host_[li]), layers_[li].act_bytes, act_file_off_[li], false, false);
     } else if (w == "act_c2g") {
-        h2d(act_restore_[li].p, act_host_[li].p, layers_[li].act_bytes);
+        h2d(act_restore_[li].p, host_act(t.id, act_host_[li]), layers_[li].act_bytes);
     } else if (w == "ckpt_g2c") {
-        d2h(ckpt_host_[k].p, ckpt_dev_[k].p, ckpt_bytes_);
+        d2h(host_act(t.id, ckpt_host_[k]), ckpt_dev_[k].p, ckpt_bytes_);
     } else if (w == "ckpt_c2s") {
-        file(*f_acts_, ckpt_host_[k].p, ckpt_bytes_, ckpt_file_off_[k], true, opt_.verify_swaps);
+        file(*f_acts_, host_act(t.id, ckpt_host_[k]), ckpt_bytes_, ckpt_file_off_[k], true, opt_.verify_swaps);
     } else if (w == "ckpt_s2c") {
-        file(*f_acts_, ckpt_host_[k].p, ckpt_bytes_, ckpt_file_off_[k], false, false);
+        file(*f_acts_, host_act(t.id, ckpt_host_[k]), ckpt_bytes_, ckpt_file_off_[k], false, false);
     } else if (w == "ckpt_c2g") {
-        h2d(ckpt_restore_[k].p, ckpt_host_[k].p, ckpt_bytes_);
+        h2d(ckpt_restore_[k].p, host_act(t.id, ckpt_host_[k]), ckpt_bytes_);
     } else if (w == "grad_g2c") {
         d2h(grad_host_[k].p, d_grads_[k], param_b);
     } else if (w == "grad_c2s") {
@@ -741,6 +869,8 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
         rep.swap_mismatches = bad;
     }
     check_cuda(cudaMemcpy(&rep.grad_sq_sum, d_norm_.p, sizeof(double), cudaMemcpyDeviceToHost), "norm");
+    rep.pinned_host_bytes = pinned_bytes_;
+    if (opt_.checksum_states && has_update_) rep.state_checksum = checksum_states();
     check_cuda(cudaMemcpy(&rep.nonfinite, d_bad_.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
 
     // real trace from the events
@@ -792,6 +922,8 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
         reference = swap_subgraph(reference, options.max_blocks);
         rep.graph = swap_subgraph(rep.graph, options.max_blocks);
     }
+    if (options.tier == StateTier::file && options.host_ring > 0)
+        add_host_ring_edges(rep.graph, options.host_ring);
     for (const Task& t : reference.tasks)
         if (t.kind == TaskKind::transfer)
             rep.reference_bytes[std::string(to_string(t.resource)) + "/" + to_string(t.payload)] += t.work;

@@ -155,3 +155,20 @@ def test_swap_only_subgraph(cuda_dev, tmp_path, placement, tier):
         assert s["io_engine"] in ("io_uring", "pread/pwrite")
         assert pb["file_write/activations"] + pb["file_read/activations"] == rb["link_ssd/activations"]
     assert "h2d/opt_states" not in pb  # no optimizer state touched
+
+
+def test_file_tier_bounded_ring_matches_host_tier(cuda_dev, tmp_path):
+    # The SSD tier proper: states/params/weights/activations staged through
+    # 2-slot pinned rings; the final states (read back from the files) must
+    # equal the host-tier run's bit for bit, with far less pinned memory.
+    sc = scenario(hardware='{"preset": "a100-12ssd", "cpu_mem": 1000000000}')
+    st, host, _, err = execute(sc, {"tier": "host", "compute_rate": RATE, "checksum_states": True,
+                                    "seed": 5})
+    assert st == 0, (err, _failing(host))
+    st, ring, _, err = execute(sc, {"tier": "file", "file_dir": str(tmp_path), "host_ring": 2,
+                                    "compute_rate": RATE, "checksum_states": True, "seed": 5})
+    assert st == 0, (err, _failing(ring))
+    assert ring["all_invariants_pass"], ring["invariants"]
+    assert ring["swap_mismatches"] == 0 and ring["swap_checks"] == L
+    assert ring["state_checksum"] == host["state_checksum"] != 0
+    assert ring["pinned_host_bytes"] < host["pinned_host_bytes"] / 2

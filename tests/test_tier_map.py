@@ -80,3 +80,18 @@ def test_swap_only_subgraph_c5():
     assert st == 0, err
     assert s["task_count"] == 4 * (2 + 8)  # + c2s and s2c legs
     assert s["mapped_bytes"]["link_ssd/activations"] == 2 * 2 * per_block
+
+
+@pytest.mark.parametrize("ring", [1, 2, 4])
+def test_host_ring_edges_keep_invariants(ring):
+    # bounded staging rings on the file tier with checkpoints on SSD: the
+    # ring-reuse edges must keep the graph a DAG the unchanged checks accept
+    st, s, _, err = execute(C1_SSD, {"dry_run": True, "tier": "file", "host_ring": ring})
+    assert st == 0, err
+    assert s["all_invariants_pass"], s["invariants"]
+    base = execute(C1_SSD, {"dry_run": True, "tier": "file"})[1]
+    # the same tasks and bytes; only extra ordering
+    assert s["task_count"] == base["task_count"]
+    assert s["mapped_bytes"] == base["mapped_bytes"]
+    # (no makespan monotonicity check: FIFO list scheduling has Graham
+    # anomalies — an extra edge can shorten the DES makespan)
