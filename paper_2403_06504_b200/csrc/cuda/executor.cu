@@ -593,7 +593,12 @@ MeasuredRates Engine::calibrate() {
         // the rates must be upper bounds for the roofline check. Requests of
         // a few MB (smaller than the calibration size) can see device-cache
         // speedups, hence the extra IO headroom applied in b200_hardware.
-        IoRequest w{&io_, f_states_->fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
+        // a scratch file in the same directory: the tier files already hold
+        // the initial states and must not be touched by the probe
+        const bool direct = opt_.direct_io && model_.hidden_dim % 64 == 0;
+        TierFile probe_file(opt_.file_dir + "/offsim_" + std::to_string(::getpid()) + "_probe.bin",
+                            round_up(bytes), direct);
+        IoRequest w{&io_, probe_file.fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
                     &io_error_text_, &io_mu_};
         IoRequest rd = w;
         rd.write = false;
@@ -609,12 +614,6 @@ MeasuredRates Engine::calibrate() {
         }
         r.file_write_bps = bytes / best_w;
         r.file_read_bps = bytes / best_r;
-        // restore the block-0 states the calibration write clobbered
-        if (h_states_[0]) {
-            IoRequest fix{&io_, f_states_->fd(), h_states_[0], round_up(12 * n_), 0, true, false,
-                          &io_error_, &io_error_text_, &io_mu_};
-            run_io(&fix);
-        }
         if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
     }
     r.compute_flops = opt_.compute_rate > 0 ? opt_.compute_rate : 0.0;
