@@ -216,6 +216,11 @@ public:
         : model_(model), plan_(plan), g_(mapped), opt_(opt), user_(chunks) {}
 
     ~Engine() {
+        // drain everything first: host IO callbacks reference io_reqs_ and
+        // the staging buffers (matters when a run throws part-way)
+        cudaSetDevice(opt_.device);
+        for (cudaStream_t s : streams_)
+            if (s) cudaStreamSynchronize(s);
         if (blas_) cublasDestroy(blas_);
         for (cudaEvent_t e : events_) cudaEventDestroy(e);
         if (base_) cudaEventDestroy(base_);
