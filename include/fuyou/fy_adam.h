@@ -102,6 +102,16 @@ uint32_t fy_adamw_workspace_floats(void);
  * grad_sq_sum is requested: the second is a one-block ordered reduction). */
 fy_status fy_adamw_chunk(const fy_adamw_args* args, void* stream);
 
+/* Same step with the all-gather fused into the epilogue:
+ * besides param_out (required: the local copy), every updated 16-bit param
+ * is stored to dst[r] (r < ndst <= 8), where dst[r] points at the start of
+ * THIS rank's slice inside rank r's full-param buffer — peer pointers
+ * (NVLink, e.g. IPC / symmetric memory) on a multi-GPU node. Replaces the
+ * separate ncclAllGather of the updated bf16 slices; the caller orders the
+ * peers' reads after this launch (event / barrier). */
+fy_status fy_adamw_chunk_gather(const fy_adamw_args* args, void* const* dst, uint32_t ndst,
+                                void* stream);
+
 /* Gradient statistics only (2 B/param read): sum of squares and non-finite
  * flag, for callers that must clip or skip before any update is applied. */
 fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad_scale,

@@ -81,6 +81,8 @@ def _load() -> C.CDLL:
         "fy_last_error": (C.c_char_p, []),
         "fy_adamw_workspace_floats": (C.c_uint32, []),
         "fy_adamw_chunk": (st, [C.POINTER(AdamwArgs), C.c_void_p]),
+        "fy_adamw_chunk_gather": (st, [C.POINTER(AdamwArgs), C.POINTER(C.c_void_p), C.c_uint32,
+                                       C.c_void_p]),
         "fy_grad_stats": (st, [C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_void_p, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p]),
         "fy_adamw_tune": (st, [C.c_int, C.c_int, C.c_int]),

@@ -24,6 +24,16 @@ AdamScalars make_scalars(float lr, float beta1, float beta2, float eps, float we
                          std::uint64_t step, int adamw_mode, int bias_correction,
                          float grad_scale);
 
+// Fused all-gather epilogue: the updated 16-bit params of this launch are
+// also stored at ptr[r] (r < count), each pointing where this rank's slice
+// starts inside rank r's full-param buffer — peer (NVLink) pointers on a
+// multi-GPU node, local buffers in single-GPU tests.
+constexpr int kMaxPeers = 8;
+struct Peers {
+    void* ptr[kMaxPeers];
+    int count;
+};
+
 struct AdamLaunch {
     float* master;
     float* m;
@@ -38,6 +48,7 @@ struct AdamLaunch {
     int accumulate_sq;
     float* workspace;    // >= kWorkspaceFloats when grad_sq_sum
     int* nonfinite;      // optional
+    Peers peers;         // optional fused gather (count 0 = off)
 };
 
 constexpr int kThreads = 256;

@@ -42,6 +42,10 @@ bool valid_param_dtype(int d) { return d == FY_BF16 || d == FY_FP16; }
 
 } // namespace
 
+namespace {
+fy_status fy_adamw_chunk_impl(const fy_adamw_args* a, void* stream, const fy::Peers* peers);
+} // namespace
+
 struct fy_pipeline {
     explicit fy_pipeline(const fy_pipeline_config& c) : impl(c) {}
     fy::ChunkPipeline impl;
@@ -57,35 +61,62 @@ uint32_t fy_adamw_workspace_floats(void) { return fy::kWorkspaceFloats; }
 
 fy_status fy_adamw_chunk(const fy_adamw_args* a, void* stream) {
     if (!a) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] { return fy_adamw_chunk_impl(a, stream, nullptr); });
+}
+
+} // extern "C"
+
+namespace {
+
+// Validation + launch shared by fy_adamw_chunk and fy_adamw_chunk_gather
+// (runs inside their guard(); CUDA failures throw fy::DeviceError).
+fy_status fy_adamw_chunk_impl(const fy_adamw_args* a, void* stream, const fy::Peers* peers) {
+    if (a->n > 0 && (!a->master || !a->exp_avg || !a->exp_avg_sq || !a->grad))
+        return fail(FY_ERR_CONFIG, "null argument");
+    if (!valid_grad_dtype(a->grad_dtype)) return fail(FY_ERR_CONFIG, "bad grad_dtype");
+    if (a->param_out && !valid_param_dtype(a->param_dtype))
+        return fail(FY_ERR_CONFIG, "param_dtype must be bf16 or fp16");
+    if (a->param_out && a->param_out == a->grad && a->grad_dtype == FY_FP32)
+        return fail(FY_ERR_CONFIG, "param_out may alias grad only for 16-bit grads");
+    if (a->grad_sq_sum && !a->workspace)
+        return fail(FY_ERR_CONFIG, "grad_sq_sum requires workspace");
+    if (a->hp.step == 0) return fail(FY_ERR_CONFIG, "step must be >= 1");
+    fy::AdamLaunch l{};
+    l.master = a->master;
+    l.m = a->exp_avg;
+    l.v = a->exp_avg_sq;
+    l.grad = a->grad;
+    l.grad_dtype = a->grad_dtype;
+    l.param = a->param_out;
+    l.param_dtype = a->param_dtype;
+    l.n = a->n;
+    l.s = fy::make_scalars(a->hp.lr, a->hp.beta1, a->hp.beta2, a->hp.eps, a->hp.weight_decay,
+                           a->hp.step, a->hp.adamw_mode, a->hp.bias_correction,
+                           a->hp.grad_scale);
+    l.grad_sq_sum = a->grad_sq_sum;
+    l.accumulate_sq = a->accumulate_sq;
+    l.workspace = a->workspace;
+    l.nonfinite = a->nonfinite_flag;
+    if (peers) l.peers = *peers;
+    fy::check_cuda(fy::launch_adamw(l, static_cast<cudaStream_t>(stream)), "fy_adamw_chunk");
+    return FY_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+fy_status fy_adamw_chunk_gather(const fy_adamw_args* a, void* const* dst, uint32_t ndst, void* stream) {
+    if (!a || (ndst > 0 && !dst)) return fail(FY_ERR_CONFIG, "null argument");
+    if (ndst > static_cast<uint32_t>(fy::kMaxPeers)) return fail(FY_ERR_CONFIG, "at most 8 destinations");
+    if (!a->param_out) return fail(FY_ERR_CONFIG, "fused gather needs param_out (the local copy)");
     return guard([&] {
-        if (a->n > 0 && (!a->master || !a->exp_avg || !a->exp_avg_sq || !a->grad))
-            return fail(FY_ERR_CONFIG, "null argument");
-        if (!valid_grad_dtype(a->grad_dtype)) return fail(FY_ERR_CONFIG, "bad grad_dtype");
-        if (a->param_out && !valid_param_dtype(a->param_dtype))
-            return fail(FY_ERR_CONFIG, "param_dtype must be bf16 or fp16");
-        if (a->param_out && a->param_out == a->grad && a->grad_dtype == FY_FP32)
-            return fail(FY_ERR_CONFIG, "param_out may alias grad only for 16-bit grads");
-        if (a->grad_sq_sum && !a->workspace)
-            return fail(FY_ERR_CONFIG, "grad_sq_sum requires workspace");
-        if (a->hp.step == 0) return fail(FY_ERR_CONFIG, "step must be >= 1");
-        fy::AdamLaunch l{};
-        l.master = a->master;
-        l.m = a->exp_avg;
-        l.v = a->exp_avg_sq;
-        l.grad = a->grad;
-        l.grad_dtype = a->grad_dtype;
-        l.param = a->param_out;
-        l.param_dtype = a->param_dtype;
-        l.n = a->n;
-        l.s = fy::make_scalars(a->hp.lr, a->hp.beta1, a->hp.beta2, a->hp.eps, a->hp.weight_decay,
-                               a->hp.step, a->hp.adamw_mode, a->hp.bias_correction,
-                               a->hp.grad_scale);
-        l.grad_sq_sum = a->grad_sq_sum;
-        l.accumulate_sq = a->accumulate_sq;
-        l.workspace = a->workspace;
-        l.nonfinite = a->nonfinite_flag;
-        fy::check_cuda(fy::launch_adamw(l, static_cast<cudaStream_t>(stream)), "fy_adamw_chunk");
-        return FY_OK;
+        for (uint32_t r = 0; r < ndst; ++r)
+            if (!dst[r]) return fail(FY_ERR_CONFIG, "null destination");
+        fy::Peers peers{};
+        peers.count = static_cast<int>(ndst);
+        for (uint32_t r = 0; r < ndst; ++r) peers.ptr[r] = dst[r];
+        return fy_adamw_chunk_impl(a, stream, &peers);
     });
 }
 

@@ -72,6 +72,30 @@ def adamw_chunk(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.T
     check(LIB.fy_adamw_chunk(C.byref(a), C.c_void_p(stream.cuda_stream)))
 
 
+def adamw_chunk_gather(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.Tensor,
+                       grad: torch.Tensor, hp: Hparams, param_out: torch.Tensor, dst_ptrs,
+                       grad_sq_sum: Optional[torch.Tensor] = None,
+                       workspace: Optional[torch.Tensor] = None,
+                       stream: Optional[torch.cuda.Stream] = None, n: Optional[int] = None) -> None:
+    """fy_adamw_chunk_gather: the step plus a fused all-gather epilogue that
+    stores the updated 16-bit params at every address in ``dst_ptrs`` (where
+    this rank's slice starts in each rank's full-param buffer)."""
+    if stream is None:
+        stream = torch.cuda.current_stream(master.device)
+    a = AdamwArgs()
+    a.master, a.exp_avg, a.exp_avg_sq = master.data_ptr(), exp_avg.data_ptr(), exp_avg_sq.data_ptr()
+    a.grad = grad.data_ptr()
+    a.grad_dtype = fy_dtype(grad.dtype)
+    a.param_out = param_out.data_ptr()
+    a.param_dtype = fy_dtype(param_out.dtype)
+    a.n = master.numel() if n is None else n
+    a.hp = hp.c()
+    a.grad_sq_sum = _ptr(grad_sq_sum)
+    a.workspace = _ptr(workspace)
+    arr = (C.c_void_p * len(dst_ptrs))(*dst_ptrs)
+    check(LIB.fy_adamw_chunk_gather(C.byref(a), arr, len(dst_ptrs), C.c_void_p(stream.cuda_stream)))
+
+
 def grad_stats(grad: torch.Tensor, grad_scale: float, grad_sq_sum: torch.Tensor,
                workspace: torch.Tensor, nonfinite: Optional[torch.Tensor] = None,
                accumulate: bool = False, stream: Optional[torch.cuda.Stream] = None) -> None:

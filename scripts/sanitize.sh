@@ -7,7 +7,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 CS=/usr/local/cuda/bin/compute-sanitizer
 SEL="bit_exact and (4099 or 1048579) or tma_bulk_path_bit_exact and 14341 or alias or nonfinite or unaligned"
-(timeout 900 $CS --tool memcheck --leak-check full --error-exitcode 9 \
+(timeout 900 $CS --tool memcheck --error-exitcode 9 \
    python -m pytest tests/test_adamw_gpu.py -q -x -k "$SEL" > $OUT/${TAG}_memcheck_kernels.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_kernels.log)
 (timeout 900 $CS --tool memcheck --error-exitcode 9 \
    python -m pytest tests/test_pipeline_gpu.py -q -x > $OUT/${TAG}_memcheck_pipeline.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_pipeline.log)
