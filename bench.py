@@ -79,6 +79,9 @@ def parse():
     ap.add_argument("--cpu-sample-chunks", type=int, default=2)
     ap.add_argument("--no-swap-sweep", action="store_true")
     ap.add_argument("--no-backward-overlap", action="store_true")
+    ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
+                    help="N>1: NCCL all-gather of the bf16 slices, or the kernel's fused "
+                         "peer-store epilogue over symmetric memory (NVLink)")
     ap.add_argument("--ssd-tier", action="store_true", help="opt-in: file-tier iteration (slow disk)")
     ap.add_argument("--layers", type=int, default=C2["layers"], help="override (debug only)")
     ap.add_argument("--hidden", type=int, default=C2["hidden"], help="override (debug only)")
@@ -162,7 +165,7 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and not dist.is_initialized():
+    if (world > 1 or getattr(args, "gather", "nccl") == "fused") and not dist.is_initialized():
         dist.init_process_group("nccl" if args.impl == "b200" else "gloo",
                                 device_id=torch.device("cuda", local) if args.impl == "b200" else None)
     return world, rank, local
@@ -430,7 +433,19 @@ def resident_phase(torch, F, args, world, rank, local):
         states.append(st)
         grads.append(g)
     full = None
-    if world > 1:
+    fused = args.gather == "fused"
+    dst_ptrs = None
+    symm = None
+    if fused:
+        # one symmetric buffer holding every chunk's full bf16 params on
+        # every rank; rank r's slice of chunk k starts at (k*world + r)*pad
+        import torch.distributed._symmetric_memory as symm_mem
+        big = symm_mem.empty(L * world * slice_pad, dtype=torch.bfloat16, device=dev)
+        symm = symm_mem.rendezvous(big, dist.group.WORLD.group_name)
+        full = [big[k * world * slice_pad:(k + 1) * world * slice_pad] for k in range(L)]
+        dst_ptrs = [[symm.buffer_ptrs[q] + 2 * (k * world + rank) * slice_pad for q in range(world)]
+                    for k in range(L)]
+    elif world > 1:
         full = [torch.empty(world * slice_pad, dtype=torch.bfloat16, device=dev) for _ in range(L)]
     ws = torch.zeros(F.optim.workspace_floats(), device=dev)
     sq = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -445,20 +460,28 @@ def resident_phase(torch, F, args, world, rank, local):
             st = states[k]
             if evs is not None:
                 evs[k][0].record(stream)
-            F.optim.adamw_chunk(st[:slice_pad], st[slice_pad:2 * slice_pad],
-                                st[2 * slice_pad:], grads[k], hp, param_out=grads[k],
-                                grad_sq_sum=sq, accumulate_sq=k > 0, workspace=ws,
-                                nonfinite=bad, stream=stream, n=cnt)
+            if fused:  # update + all-gather in one kernel (peer stores)
+                F.optim.adamw_chunk_gather(st[:slice_pad], st[slice_pad:2 * slice_pad],
+                                           st[2 * slice_pad:], grads[k], hp, grads[k], dst_ptrs[k],
+                                           grad_sq_sum=sq, workspace=ws, stream=stream, n=cnt)
+            else:
+                F.optim.adamw_chunk(st[:slice_pad], st[slice_pad:2 * slice_pad],
+                                    st[2 * slice_pad:], grads[k], hp, param_out=grads[k],
+                                    grad_sq_sum=sq, accumulate_sq=k > 0, workspace=ws,
+                                    nonfinite=bad, stream=stream, n=cnt)
             if evs is not None:
                 evs[k][1].record(stream)
-            if world > 1:
+            if world > 1 and not fused:
                 done = torch.cuda.Event()
                 done.record(stream)
                 comm.wait_event(done)
                 with torch.cuda.stream(comm):
                     dist.all_gather_into_tensor(full[k], grads[k])
-        if world > 1:
+        if world > 1 and not fused:
             stream.wait_stream(comm)
+        if fused:
+            with torch.cuda.stream(stream):
+                symm.barrier(channel=0)  # peers' stores landed before the params are used
 
     for w in range(args.warmup):
         one_step(w)
@@ -879,7 +902,8 @@ def main():
                         f"{12 * args.hidden * args.hidden} params), one AdamW step, states "
                         "device-resident (bf16 grads -> bf16 params in place)",
             "params": P, "chunk_params": 12 * args.hidden * args.hidden,
-            "parallelism": f"shard{world}" if world > 1 else "single",
+            "parallelism": (f"shard{world}" if world > 1 else "single")
+                           + ("+fused-gather" if args.gather == "fused" else ""),
             "l2": "inputs larger than L2 (176 GB resident)",
             "hparams": "lr 1e-4, betas (0.9, 0.95), eps 1e-8, wd 0.1, adamw, bias corr",
             "gb_per_s_at_28B": res["value"] * BYTES_RESIDENT / 1e9,
