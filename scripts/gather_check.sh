@@ -11,4 +11,4 @@ mkdir -p $OUT
 (timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
    --master-port 29518 bench.py --gpus 1 --impl reference --steps 5 --warmup 3 \
    > $OUT/${TAG}_reference_arm.json 2> $OUT/${TAG}_reference_arm.err; echo "rc=$?" >> $OUT/${TAG}_reference_arm.err)
-tail -3 $OUT/${TAG}_fused_gather.err $OUT/${TAG}_reference_arm.err
+tail -n 3 $OUT/${TAG}_fused_gather.err $OUT/${TAG}_reference_arm.err
