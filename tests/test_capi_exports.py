@@ -58,3 +58,66 @@ def test_errors_are_status_codes():
     assert LIB.fy_adamw_chunk(None, None) == FY_ERR_CONFIG
     assert LIB.fy_last_error() == b"null argument"
     assert LIB.fy_version().startswith(b"0.")
+
+
+def test_argument_validation_without_gpu():
+    """Every fy_* entry point validates its arguments before touching the
+    device, with the reference C ABI's conventions (status codes, thread-local
+    last error) — so these run on a CPU-only machine."""
+    from paper_2403_06504_b200._lib import (LIB, AdamwArgs, AdamHparams, FY_ERR_CONFIG,
+                                            PipelineConfig)
+    a = AdamwArgs()
+    a.n = 16
+    a.master = a.exp_avg = a.exp_avg_sq = a.grad = 0x1000
+    a.hp = AdamHparams(1e-4, 0.9, 0.95, 1e-8, 0.1, 0, 1, 1, 1.0)  # step 0
+    assert LIB.fy_adamw_chunk(C.byref(a), None) == FY_ERR_CONFIG
+    assert b"step" in LIB.fy_last_error()
+    a.hp.step = 10
+    a.grad_dtype = 7
+    assert LIB.fy_adamw_chunk(C.byref(a), None) == FY_ERR_CONFIG
+    assert b"grad_dtype" in LIB.fy_last_error()
+    a.grad_dtype = 0
+    a.grad_sq_sum = 0x2000  # without workspace
+    assert LIB.fy_adamw_chunk(C.byref(a), None) == FY_ERR_CONFIG
+    assert b"workspace" in LIB.fy_last_error()
+    dst = (C.c_void_p * 9)(*([0x3000] * 9))
+    a.grad_sq_sum = None
+    a.param_out = 0x4000
+    assert LIB.fy_adamw_chunk_gather(C.byref(a), dst, 9, None) == FY_ERR_CONFIG
+    assert b"8" in LIB.fy_last_error()
+    a.param_out = None
+    assert LIB.fy_adamw_chunk_gather(C.byref(a), dst, 2, None) == FY_ERR_CONFIG
+    assert b"param_out" in LIB.fy_last_error()
+    assert LIB.fy_adamw_tune(2, 3, 0) == FY_ERR_CONFIG
+    assert LIB.fy_adamw_tune(0, 3, 0) == FY_ERR_CONFIG
+    assert LIB.fy_adamw_tune(1, 5, 0) == FY_ERR_CONFIG
+    assert LIB.fy_adamw_tune(1, 3, 2) == FY_ERR_CONFIG
+    h = C.c_void_p()
+    cfg = PipelineConfig(0, 1024, 1, 0, 0, 0, 1, 0, 0)
+    assert LIB.fy_pipeline_create(C.byref(cfg), C.byref(h)) == FY_ERR_CONFIG
+    assert b"slots" in LIB.fy_last_error()
+    cfg = PipelineConfig(0, 0, 3, 0, 0, 0, 1, 0, 0)
+    assert LIB.fy_pipeline_create(C.byref(cfg), C.byref(h)) == FY_ERR_CONFIG
+    cfg = PipelineConfig(0, 1024, 3, 0, 2, 0, 1, 0, 0)  # fp32 params
+    assert LIB.fy_pipeline_create(C.byref(cfg), C.byref(h)) == FY_ERR_CONFIG
+    assert LIB.fy_pipeline_step(None, None, 0, None, 0) == FY_ERR_CONFIG
+    assert LIB.fy_pipeline_wait(None, None, None) == FY_ERR_CONFIG
+    assert LIB.fy_host_alloc(16, None) == FY_ERR_CONFIG
+
+
+def test_graph_execute_rejects_bad_input_without_gpu():
+    from paper_2403_06504_b200._lib import LIB, Chunk
+    LIB.fy_graph_execute.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(Chunk), C.c_uint32,
+                                     C.POINTER(C.c_void_p)]
+    LIB.offsim_last_error.restype = C.c_char_p
+    out = C.c_void_p()
+    assert LIB.fy_graph_execute(b"{bad", None, None, 0, C.byref(out)) == 2
+    assert LIB.fy_graph_execute(None, None, None, 0, C.byref(out)) == 2
+    sc = (b'{"schema_version": 1, "model": {"num_layers": 2, "num_heads": 4, "hidden_dim": 64},'
+          b' "hardware": "a100-12ssd"}')
+    arr = (Chunk * 2)()
+    arr[0].n = arr[1].n = 12 * 64 * 64 + 1  # wrong chunk size
+    assert LIB.fy_graph_execute(sc, None, arr, 2, C.byref(out)) == 2
+    assert b"12*h^2" in LIB.offsim_last_error()
+    assert LIB.fy_graph_execute(sc, b'{"tier": "disk"}', None, 0, C.byref(out)) == 2
+    assert not out.value
