@@ -84,6 +84,9 @@ struct ExecOptions {
     // plan places them on SSD), so host memory no longer scales with the
     // model. Ring reuse is expressed as graph edges (add_host_ring_edges).
     std::uint32_t host_ring = 0;
+    // host_ring "auto": per-ring depths from the reference schedule's own
+    // windows (host_ring_depths) instead of one uniform N.
+    bool host_ring_auto = false;
     // Report an FNV-1a checksum of every chunk's final [master|m|v].
     bool checksum_states = false;
 };
@@ -110,6 +113,26 @@ TaskGraph map_graph_for_b200(const TaskGraph& graph, StateTier tier,
 // (param_d2h .. param_c2s), weight fetches (p_s2c .. p_c2g) and, when
 // checkpoints live on SSD, activation transfers (g2c .. c2s, s2c .. c2g).
 void add_host_ring_edges(TaskGraph& mapped, std::uint32_t slots);
+
+// Slot counts of the four staging rings (0 = that ring is unused).
+struct RingDepths {
+    std::uint32_t states = 0;  // optimizer groups [master|m|v]
+    std::uint32_t params = 0;  // bf16 param write-backs
+    std::uint32_t weights = 0; // layer weight fetches (p_s2c .. p_c2g)
+    std::uint32_t acts = 0;    // activations / checkpoints, placement = ssd
+};
+void add_host_ring_edges(TaskGraph& mapped, const RingDepths& depths);
+
+// Ring depths of `mapped` under `opts` (all zero unless tier = file and
+// host_ring > 0 or host_ring_auto). Uniform: host_ring slots per ring. Auto,
+// from the windows build_schedule sized (task_graph.cpp:145-224, recorded in
+// the graph header): weights = the CPU stage window in blocks
+// (ceil(cpu_stage_window_layers / 4)); acts = the offload window
+// (offload_window_blocks) times the activation units per block; states and
+// params = the device staging slots (the optimizer's depth-2 read gate plus
+// one write-back in flight). Every depth is at least 2 and at most the
+// number of uses of its ring.
+RingDepths host_ring_depths(const TaskGraph& mapped, const ExecOptions& opts);
 
 // The activation-swap path of a (mapped) graph: every task with payload
 // activations whose block index is < max_blocks (0 = all), dependencies
@@ -145,6 +168,7 @@ struct ExecReport {
     std::uint32_t kernel_launches = 0;
     std::string io_engine; // "io_uring" | "pread/pwrite" (file tier)
     std::uint64_t pinned_host_bytes = 0;  // host staging the run allocated
+    RingDepths host_ring;                 // staging ring depths (file tier)
     std::uint64_t state_checksum = 0;     // checksum_states
 };
 

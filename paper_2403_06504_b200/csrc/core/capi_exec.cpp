@@ -61,7 +61,13 @@ ParsedOptions parse_options(const char* text) {
         out.dry_run = doc.value("dry_run", false);
         out.variant = doc.value("variant", std::string());
         o.compute_mode = doc.value("compute_mode", o.compute_mode);
-        o.host_ring = doc.value("host_ring", o.host_ring);
+        if (doc.contains("host_ring") && doc.at("host_ring").is_string()) {
+            if (doc.at("host_ring").get<std::string>() != "auto")
+                throw ConfigError("exec options: host_ring must be a slot count or 'auto'");
+            o.host_ring_auto = true;
+        } else {
+            o.host_ring = doc.value("host_ring", o.host_ring);
+        }
         o.checksum_states = doc.value("checksum_states", o.checksum_states);
         o.swap_only = doc.value("swap_only", o.swap_only);
         o.max_blocks = doc.value("max_blocks", o.max_blocks);
@@ -98,6 +104,10 @@ json bytes_json(const std::map<std::string, double>& m) {
     json j = json::object();
     for (const auto& [k, v] : m) j[k] = v;
     return j;
+}
+
+json rings_json(const RingDepths& d) {
+    return json{{"states", d.states}, {"params", d.params}, {"weights", d.weights}, {"acts", d.acts}};
 }
 
 json trace_stats(const SimTrace& t) {
@@ -159,6 +169,7 @@ std::string exec_summary_json(const ExecReport& r) {
         {"kernel_launches", r.kernel_launches},
         {"io_engine", r.io_engine},
         {"pinned_host_bytes", r.pinned_host_bytes},
+        {"host_ring", rings_json(r.host_ring)},
         {"state_checksum", r.state_checksum},
         {"invariants", checks},
         {"all_invariants_pass", r.invariants.all_pass && r.swap_mismatches == 0},
@@ -187,7 +198,8 @@ std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVar
     const TaskGraph ref = build_schedule(s.model, s.hardware, plan, v);
     TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots);
     if (po.exec.swap_only) mapped = swap_subgraph(mapped, po.exec.max_blocks);
-    if (po.exec.tier == StateTier::file && po.exec.host_ring > 0) add_host_ring_edges(mapped, po.exec.host_ring);
+    const RingDepths rings = host_ring_depths(mapped, po.exec);
+    add_host_ring_edges(mapped, rings);
     MeasuredRates nominal;
     nominal.h2d_bps = nominal.d2h_bps = 55e9;
     nominal.file_read_bps = nominal.file_write_bps = po.exec.tier == StateTier::file ? 2e9 : 0.0;
@@ -219,6 +231,10 @@ std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVar
                       {"reference_task_count", ref.tasks.size()},
                       {"task_count", mapped.tasks.size()},
                       {"inserted_tasks", inserted},
+                      {"host_ring", rings_json(rings)},
+                      {"windows", json{{"prefetch_window_layers", mapped.header.prefetch_window_layers},
+                                       {"offload_window_blocks", mapped.header.offload_window_blocks},
+                                       {"cpu_stage_window_layers", mapped.header.cpu_stage_window_layers}}},
                       {"reference_bytes", bytes_json(ref_bytes)},
                       {"mapped_bytes", bytes_json(mapped_bytes)},
                       {"planned", trace_stats(tr)},

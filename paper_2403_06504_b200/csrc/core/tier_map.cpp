@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <vector>
 #include <string>
 
 namespace offsim {
@@ -153,14 +155,19 @@ TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t 
     return out;
 }
 
-void add_host_ring_edges(TaskGraph& g, std::uint32_t slots) {
-    if (slots == 0) return;
+namespace {
+
+struct RingUse {
+    std::uint32_t first, last;
+};
+struct RingUses {
+    std::vector<RingUse> states, params, weights, acts;
+};
+
+// Uses of each staging ring in task id order: (first task, last task).
+RingUses ring_uses(const TaskGraph& g) {
     std::map<std::string, std::uint32_t> by_name;
     for (const Task& t : g.tasks) by_name[t.name] = t.id;
-    struct Use {
-        std::uint32_t first, last;
-    };
-    std::vector<Use> states, params, weights, acts;
     const bool acts_on_ssd = g.header.checkpoint_location == "ssd";
     auto partner = [&](const std::string& name, const char* from, const char* to) {
         std::string other = name;
@@ -168,19 +175,31 @@ void add_host_ring_edges(TaskGraph& g, std::uint32_t slots) {
         const auto it = by_name.find(other);
         return it == by_name.end() ? 0xffffffffu : it->second;
     };
+    RingUses u;
     for (const Task& t : g.tasks) {
         const std::string& n = t.name;
-        if (starts_with(n, "opt state_s2c ")) states.push_back({t.id, partner(n, "state_s2c", "state_c2s")});
-        else if (starts_with(n, "opt param_d2h ")) params.push_back({t.id, partner(n, "param_d2h", "param_c2s")});
-        else if (n.find(" p_s2c ") != std::string::npos) weights.push_back({t.id, partner(n, "p_s2c", "p_c2g")});
+        if (starts_with(n, "opt state_s2c ")) u.states.push_back({t.id, partner(n, "state_s2c", "state_c2s")});
+        else if (starts_with(n, "opt param_d2h ")) u.params.push_back({t.id, partner(n, "param_d2h", "param_c2s")});
+        else if (n.find(" p_s2c ") != std::string::npos) u.weights.push_back({t.id, partner(n, "p_s2c", "p_c2g")});
         else if (acts_on_ssd && (starts_with(n, "fwd act_g2c ") || starts_with(n, "fwd ckpt_g2c ")))
-            acts.push_back({t.id, partner(n, "_g2c", "_c2s")});
+            u.acts.push_back({t.id, partner(n, "_g2c", "_c2s")});
         else if (acts_on_ssd && (starts_with(n, "bwd act_s2c ") || starts_with(n, "bwd ckpt_s2c ")))
-            acts.push_back({t.id, partner(n, "_s2c", "_c2g")});
+            u.acts.push_back({t.id, partner(n, "_s2c", "_c2g")});
     }
-    for (std::vector<Use>* uses : {&states, &params, &weights, &acts}) {
+    return u;
+}
+
+} // namespace
+
+void add_host_ring_edges(TaskGraph& g, const RingDepths& depths) {
+    RingUses u = ring_uses(g);
+    const std::pair<std::vector<RingUse>*, std::uint32_t> rings[] = {
+        {&u.states, depths.states}, {&u.params, depths.params},
+        {&u.weights, depths.weights}, {&u.acts, depths.acts}};
+    for (const auto& [uses, slots] : rings) {
+        if (slots == 0) continue;
         for (std::size_t k = slots; k < uses->size(); ++k) {
-            const Use& prev = (*uses)[k - slots];
+            const RingUse& prev = (*uses)[k - slots];
             if (prev.last == 0xffffffffu) throw InvariantError("host ring: unpaired task '" + g.tasks[prev.first].name + "'");
             Task& t = g.tasks[(*uses)[k].first];
             if (prev.last >= t.id) throw InvariantError("host ring edge would not be topological at '" + t.name + "'");
@@ -189,6 +208,32 @@ void add_host_ring_edges(TaskGraph& g, std::uint32_t slots) {
             t.deps.erase(std::unique(t.deps.begin(), t.deps.end()), t.deps.end());
         }
     }
+}
+
+void add_host_ring_edges(TaskGraph& g, std::uint32_t slots) {
+    add_host_ring_edges(g, RingDepths{slots, slots, slots, slots});
+}
+
+RingDepths host_ring_depths(const TaskGraph& g, const ExecOptions& o) {
+    if (o.tier != StateTier::file || (o.host_ring == 0 && !o.host_ring_auto)) return {};
+    if (!o.host_ring_auto) return RingDepths{o.host_ring, o.host_ring, o.host_ring, o.host_ring};
+    const RingUses u = ring_uses(g);
+    auto clamp = [](std::uint64_t want, std::size_t uses) {
+        if (uses == 0) return 0u;
+        return static_cast<std::uint32_t>(std::min<std::uint64_t>(std::max<std::uint64_t>(want, 2), uses));
+    };
+    const TraceHeader& h = g.header;
+    // activation units per block: the checkpoint plus the swapped linears
+    std::uint64_t blocks = 0;
+    for (const Task& t : g.tasks)
+        if (starts_with(t.name, "fwd ckpt_g2c ")) ++blocks;
+    const std::uint64_t act_units = blocks ? (u.acts.size() / 2 + blocks - 1) / blocks : 1;
+    RingDepths d;
+    d.states = clamp(o.state_slots, u.states.size());
+    d.params = clamp(o.state_slots, u.params.size());
+    d.weights = clamp((h.cpu_stage_window_layers + 3) / 4, u.weights.size());
+    d.acts = clamp(static_cast<std::uint64_t>(h.offload_window_blocks) * act_units, u.acts.size());
+    return d;
 }
 
 TaskGraph swap_subgraph(const TaskGraph& in, std::uint32_t max_blocks) {

@@ -252,8 +252,9 @@ private:
     bool file_tier_ = false;
     bool has_update_ = false;
     bool has_weights_ = false;
-    // bounded pinned staging rings (file tier, host_ring > 0)
+    // bounded pinned staging rings (file tier, host_ring > 0 or auto)
     bool ring_ = false;
+    RingDepths depths_;
     bool acts_on_ssd_ = false;
     std::vector<Pinned> state_ring_, param_ring_, weight_ring_, act_ring_;
     std::map<std::uint32_t, int> ring_slot_; // task id -> ring slot
@@ -366,7 +367,8 @@ void Engine::setup() {
         if (p.what.rfind("ckpt_", 0) == 0) ckpt_used[p.block] = true;
     }
     const bool need_chunks = has_update_ || has_weights_;
-    ring_ = file_tier_ && opt_.host_ring > 0;
+    depths_ = host_ring_depths(g_, opt_);
+    ring_ = depths_.states || depths_.params || depths_.weights || depths_.acts;
     acts_on_ssd_ = g_.header.checkpoint_location == "ssd";
     if (ring_ && user_) throw ConfigError("executor: host_ring stages synthetic states only (offsim_execute)");
     h_states_.assign(blocks_, nullptr);
@@ -439,20 +441,15 @@ void Engine::setup() {
         for (std::uint32_t k = 0; k < blocks_; ++k) grad_host_.push_back(pin(round_up(param_b)));
 
     if (ring_) {
-        const std::uint32_t R = opt_.host_ring;
         std::uint64_t max_w = 0, max_act = ckpt_bytes_;
         for (std::size_t i = 0; i < layers_.size(); ++i) {
             max_w = std::max(max_w, layers_[i].param_bytes);
             if (swapped_[i]) max_act = std::max(max_act, layers_[i].act_bytes);
         }
-        for (std::uint32_t r = 0; r < R; ++r) {
-            if (has_update_) {
-                state_ring_.push_back(pin(round_up(state_b)));
-                param_ring_.push_back(pin(round_up(param_b)));
-            }
-            if (has_weights_) weight_ring_.push_back(pin(round_up(max_w)));
-            if (acts_on_ssd_) act_ring_.push_back(pin(round_up(max_act)));
-        }
+        for (std::uint32_t r = 0; r < depths_.states; ++r) state_ring_.push_back(pin(round_up(state_b)));
+        for (std::uint32_t r = 0; r < depths_.params; ++r) param_ring_.push_back(pin(round_up(param_b)));
+        for (std::uint32_t r = 0; r < depths_.weights; ++r) weight_ring_.push_back(pin(round_up(max_w)));
+        for (std::uint32_t r = 0; r < depths_.acts; ++r) act_ring_.push_back(pin(round_up(max_act)));
         assign_ring_slots();
     }
 
@@ -646,7 +643,6 @@ MeasuredRates Engine::calibrate() {
 void Engine::assign_ring_slots() {
     std::map<std::string, std::uint32_t> id_of;
     for (const Task& t : g_.tasks) id_of[t.name] = t.id;
-    const std::uint32_t R = opt_.host_ring;
     std::uint32_t ns = 0, np = 0, nw = 0, na = 0;
     auto tie = [&](const std::string& name, int slot) {
         const auto it = id_of.find(name);
@@ -659,23 +655,23 @@ void Engine::assign_ring_slots() {
     for (const Task& t : g_.tasks) {
         const std::string& n = t.name;
         if (n.rfind("opt state_s2c ", 0) == 0) {
-            const int slot = static_cast<int>(ns++ % R);
+            const int slot = static_cast<int>(ns++ % depths_.states);
             for (const char* w : {"state_s2c", "state_h2d", "state_d2h", "state_c2s"})
                 tie(swap_name(n, "state_s2c", w), slot);
         } else if (n.rfind("opt param_d2h ", 0) == 0) {
-            const int slot = static_cast<int>(np++ % R);
+            const int slot = static_cast<int>(np++ % depths_.params);
             tie(n, slot);
             tie(swap_name(n, "param_d2h", "param_c2s"), slot);
         } else if (n.find(" p_s2c ") != std::string::npos) {
-            const int slot = static_cast<int>(nw++ % R);
+            const int slot = static_cast<int>(nw++ % depths_.weights);
             tie(n, slot);
             tie(swap_name(n, "p_s2c", "p_c2g"), slot);
         } else if (acts_on_ssd_ && (n.rfind("fwd act_g2c ", 0) == 0 || n.rfind("fwd ckpt_g2c ", 0) == 0)) {
-            const int slot = static_cast<int>(na++ % R);
+            const int slot = static_cast<int>(na++ % depths_.acts);
             tie(n, slot);
             tie(swap_name(n, "_g2c", "_c2s"), slot);
         } else if (acts_on_ssd_ && (n.rfind("bwd act_s2c ", 0) == 0 || n.rfind("bwd ckpt_s2c ", 0) == 0)) {
-            const int slot = static_cast<int>(na++ % R);
+            const int slot = static_cast<int>(na++ % depths_.acts);
             tie(n, slot);
             tie(swap_name(n, "_s2c", "_c2g"), slot);
         }
@@ -926,8 +922,8 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
         reference = swap_subgraph(reference, options.max_blocks);
         rep.graph = swap_subgraph(rep.graph, options.max_blocks);
     }
-    if (options.tier == StateTier::file && options.host_ring > 0)
-        add_host_ring_edges(rep.graph, options.host_ring);
+    rep.host_ring = host_ring_depths(rep.graph, options);
+    add_host_ring_edges(rep.graph, rep.host_ring);
     for (const Task& t : reference.tasks)
         if (t.kind == TaskKind::transfer)
             rep.reference_bytes[std::string(to_string(t.resource)) + "/" + to_string(t.payload)] += t.work;

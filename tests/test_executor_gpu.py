@@ -165,10 +165,15 @@ def test_file_tier_bounded_ring_matches_host_tier(cuda_dev, tmp_path):
     st, host, _, err = execute(sc, {"tier": "host", "compute_rate": RATE, "checksum_states": True,
                                     "seed": 5})
     assert st == 0, (err, _failing(host))
-    st, ring, _, err = execute(sc, {"tier": "file", "file_dir": str(tmp_path), "host_ring": 2,
-                                    "compute_rate": RATE, "checksum_states": True, "seed": 5})
-    assert st == 0, (err, _failing(ring))
-    assert ring["all_invariants_pass"], ring["invariants"]
-    assert ring["swap_mismatches"] == 0 and ring["swap_checks"] == L
-    assert ring["state_checksum"] == host["state_checksum"] != 0
-    assert ring["pinned_host_bytes"] < host["pinned_host_bytes"] / 2
+    for depth in (2, "auto"):
+        st, ring, _, err = execute(sc, {"tier": "file", "file_dir": str(tmp_path), "host_ring": depth,
+                                        "compute_rate": RATE, "checksum_states": True, "seed": 5})
+        assert st == 0, (err, _failing(ring))
+        assert ring["all_invariants_pass"], ring["invariants"]
+        assert ring["swap_mismatches"] == 0 and ring["swap_checks"] == L
+        assert ring["state_checksum"] == host["state_checksum"] != 0
+        if depth == 2:
+            assert ring["host_ring"] == {"states": 2, "params": 2, "weights": 2, "acts": 2}
+            assert ring["pinned_host_bytes"] < host["pinned_host_bytes"] / 2
+        else:  # depths from the reference schedule's windows
+            assert ring["host_ring"]["states"] == 3 and ring["host_ring"]["weights"] >= 2

@@ -95,3 +95,24 @@ def test_host_ring_edges_keep_invariants(ring):
     assert s["mapped_bytes"] == base["mapped_bytes"]
     # (no makespan monotonicity check: FIFO list scheduling has Graham
     # anomalies — an extra edge can shorten the DES makespan)
+
+
+def test_host_ring_auto_follows_reference_windows():
+    # "auto": ring depths come from the windows build_schedule sized
+    # (task_graph.cpp:145-224) — weights = the CPU stage window in blocks,
+    # activations = the offload window x units per block, states/params =
+    # the device staging slots — clamped to [2, uses]
+    st, s, _, err = execute(C1_SSD, {"dry_run": True, "tier": "file", "host_ring": "auto"})
+    assert st == 0, err
+    assert s["all_invariants_pass"], s["invariants"]
+    w, r = s["windows"], s["host_ring"]
+    assert r["states"] == r["params"] == 3
+    assert r["weights"] == min(max((w["cpu_stage_window_layers"] + 3) // 4, 2), 2 * 4 * 12)
+    assert 2 <= r["acts"] <= 2 * (12 * 4 + 12)
+    assert r["acts"] >= min(w["offload_window_blocks"], 24)
+    st, s4, _, _ = execute(C1_SSD, {"dry_run": True, "tier": "file", "host_ring": 4})
+    assert s4["host_ring"] == {"states": 4, "params": 4, "weights": 4, "acts": 4}
+    st, s0, _, _ = execute(C1_SSD, {"dry_run": True, "tier": "host", "host_ring": "auto"})
+    assert s0["host_ring"] == {"states": 0, "params": 0, "weights": 0, "acts": 0}
+    st, _, _, err = execute(C1_SSD, {"dry_run": True, "tier": "file", "host_ring": "many"})
+    assert st == 2 and "auto" in err
