@@ -217,6 +217,29 @@ def cpu_oracle_rate(chunk: int, nchunks: int, target_s: float = 12.0, max_reps: 
     return rate, threads, sample
 
 
+def host_info():
+    """The host the CPU arm ran on (SURVEY §8d asks for socket x core counts)."""
+    info = {"threads": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            txt = f.read()
+        names = [ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("model name")]
+        sockets = {ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("physical id")}
+        cores = {ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("core id")}
+        info.update(cpu_model=names[0] if names else None, sockets=len(sockets) or None,
+                    cores_per_socket=len(cores) or None,
+                    avx512="avx512f" in txt)
+        info["numa_nodes"] = len([d for d in os.listdir("/sys/devices/system/node")
+                                  if d.startswith("node") and d[4:].isdigit()])
+    except OSError:
+        pass
+    return info
+
+
+# the reference prices the optimizer step at cpu_opt_tput (presets.cpp:45)
+REFERENCE_MODEL_RATE = 1e9
+
+
 def torch_fused_cpu_rate(chunk: int, reps: int = 3):
     import torch
     p = torch.nn.Parameter(torch.randn(chunk) * 0.02)
@@ -818,7 +841,8 @@ def run_reference(args):
                    "params": args.layers * N, "chunk_params": N,
                    "gb_per_s_at_28B": rate * 28 / 1e9},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "host": host_info(),
+                         "reference_model_rate": REFERENCE_MODEL_RATE},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -849,7 +873,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, threads, sample = cpu_oracle_rate(12 * args.hidden * args.hidden,
                                                 args.cpu_sample_chunks)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+               "host": host_info(), "reference_model_rate": REFERENCE_MODEL_RATE}
         try:
             cpu["torch_adamw_fused_cpu"] = torch_fused_cpu_rate(12 * args.hidden * args.hidden)
         except Exception as e:  # informational only
