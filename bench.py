@@ -27,8 +27,11 @@ buffer becomes the updated bf16 params, task_graph.cpp:493-495).
            on a bounded sample of the same chunks.
 
 N>1 (torchrun): every chunk is sharded across ranks (fy_shard_range, 8-elem
-aligned slices); each rank updates its slice; the updated bf16 slices are
-all-gathered over NCCL per chunk (the only data-path collective).
+aligned slices); each rank updates its slice; the updated bf16 slices reach
+every rank through the kernel's fused epilogue (peer stores into a torch
+symmetric-memory buffer over NVLink; `--gather auto`, the default) or an NCCL
+all-gather per chunk (`--gather nccl`, or auto when symmetric memory is
+unavailable) — the only data-path exchange.
 `--impl reference`: times the reference's CPU optimizer path (the oracle port
 of DeepSpeed CPU Adam, all host threads) on rank 0 only.
 """
@@ -79,9 +82,10 @@ def parse():
     ap.add_argument("--cpu-sample-chunks", type=int, default=2)
     ap.add_argument("--no-swap-sweep", action="store_true")
     ap.add_argument("--no-backward-overlap", action="store_true")
-    ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
-                    help="N>1: NCCL all-gather of the bf16 slices, or the kernel's fused "
-                         "peer-store epilogue over symmetric memory (NVLink)")
+    ap.add_argument("--gather", choices=["auto", "nccl", "fused"], default="auto",
+                    help="N>1: the kernel's fused peer-store epilogue over symmetric memory "
+                         "(NVLink), or an NCCL all-gather of the bf16 slices; auto = fused "
+                         "when torch symmetric memory rendezvous works, else NCCL (recorded)")
     ap.add_argument("--ssd-tier", action="store_true", help="opt-in: file-tier iteration (slow disk)")
     ap.add_argument("--layers", type=int, default=C2["layers"], help="override (debug only)")
     ap.add_argument("--hidden", type=int, default=C2["hidden"], help="override (debug only)")
@@ -456,19 +460,26 @@ def resident_phase(torch, F, args, world, rank, local):
         states.append(st)
         grads.append(g)
     full = None
-    fused = args.gather == "fused"
+    fused = args.gather == "fused" or (args.gather == "auto" and world > 1)
+    gather_note = None
     dst_ptrs = None
     symm = None
     if fused:
         # one symmetric buffer holding every chunk's full bf16 params on
         # every rank; rank r's slice of chunk k starts at (k*world + r)*pad
-        import torch.distributed._symmetric_memory as symm_mem
-        big = symm_mem.empty(L * world * slice_pad, dtype=torch.bfloat16, device=dev)
-        symm = symm_mem.rendezvous(big, dist.group.WORLD.group_name)
-        full = [big[k * world * slice_pad:(k + 1) * world * slice_pad] for k in range(L)]
-        dst_ptrs = [[symm.buffer_ptrs[q] + 2 * (k * world + rank) * slice_pad for q in range(world)]
-                    for k in range(L)]
-    elif world > 1:
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            big = symm_mem.empty(L * world * slice_pad, dtype=torch.bfloat16, device=dev)
+            symm = symm_mem.rendezvous(big, dist.group.WORLD.group_name)
+            full = [big[k * world * slice_pad:(k + 1) * world * slice_pad] for k in range(L)]
+            dst_ptrs = [[symm.buffer_ptrs[q] + 2 * (k * world + rank) * slice_pad
+                         for q in range(world)] for k in range(L)]
+        except Exception as e:  # auto: the NCCL all-gather instead (both are device paths)
+            if args.gather == "fused":
+                raise
+            fused, symm, gather_note = False, None, f"symmetric memory unavailable ({e}); NCCL"
+            torch.cuda.empty_cache()
+    if world > 1 and not fused:
         full = [torch.empty(world * slice_pad, dtype=torch.bfloat16, device=dev) for _ in range(L)]
     ws = torch.zeros(F.optim.workspace_floats(), device=dev)
     sq = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -541,6 +552,8 @@ def resident_phase(torch, F, args, world, rank, local):
         "launches": args.steps * L * 2,  # fused Adam kernel + 1-block ordered norm reduction
         "grad_sq_sum": float(sq.item()),
         "nonfinite": int(bad.item()),
+        "gather": ("fused" if fused else "nccl") if world > 1 or fused else None,
+        "gather_note": gather_note,
     }
 
     if not args.no_e2e:
@@ -567,11 +580,15 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
     for p in hbuf:
         arr = np.ctypeslib.as_array((C.c_uint16 * n).from_address(p.value))
         arr[:] = 0x3A83
+    # N>1: the kernel also writes this rank's params into its own slice of
+    # the chunk's full-param buffer on the device, and an in-place NCCL
+    # all-gather assembles the rest (no extra host round trip)
+    rank = dist.get_rank() if world > 1 else 0
     pipe = F.optim.ChunkPipeline(n, slots=3, grads_on_host=True, params_to_host=True,
-                                 states_on_device=True)
-    chunks = [dict(n=n, h_states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value)
+                                 keep_params_on_device=world > 1, states_on_device=True)
+    chunks = [dict(n=n, h_states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value,
+                   d_param=full[k][rank * n:(rank + 1) * n].data_ptr() if world > 1 else None)
               for k in range(L)]
-    staging = torch.empty(n, dtype=torch.bfloat16, device="cuda") if world > 1 else None
     hp = F.optim.Hparams()
 
     def step(i):
@@ -580,10 +597,7 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
         pipe.wait()
         if world > 1:  # assemble the full bf16 params on every rank (NVLink)
             for k in range(L):
-                host = torch.from_numpy(np.ctypeslib.as_array(
-                    (C.c_int16 * n).from_address(hbuf[k].value))).view(torch.bfloat16)
-                staging.copy_(host, non_blocking=True)
-                dist.all_gather_into_tensor(full[k], staging)
+                dist.all_gather_into_tensor(full[k], full[k][rank * n:(rank + 1) * n])
             torch.cuda.synchronize()
 
     for w in range(args.warmup):
@@ -606,7 +620,7 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
         "link_gbs_each_way": 2 * L * n * args.steps / el / 1e9,
         "path": "fy_pipeline_step (C ABI): host bf16 grads H2D -> fused AdamW on HBM-resident "
                 "states -> bf16 params D2H into the same host buffer; wall clock"
-                + ("; + NCCL all-gather of the bf16 slices" if world > 1 else ""),
+                + ("; + in-place NCCL all-gather of the device-side bf16 slices" if world > 1 else ""),
         "launches": args.steps * L * 2,
     }
 
@@ -928,7 +942,8 @@ def main():
                         "device-resident (bf16 grads -> bf16 params in place)",
             "params": P, "chunk_params": 12 * args.hidden * args.hidden,
             "parallelism": (f"shard{world}" if world > 1 else "single")
-                           + ("+fused-gather" if args.gather == "fused" else ""),
+                           + (f"+{res['gather']}-gather" if res.get("gather") else ""),
+            "gather_note": res.get("gather_note"),
             "l2": "inputs larger than L2 (176 GB resident)",
             "hparams": "lr 1e-4, betas (0.9, 0.95), eps 1e-8, wd 0.1, adamw, bias corr",
             "gb_per_s_at_28B": res["value"] * BYTES_RESIDENT / 1e9,

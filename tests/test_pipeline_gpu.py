@@ -125,3 +125,33 @@ def test_pipeline_waits_for_grad_ready_events(cuda_dev):
         O.adamw_step(mst, mm, vv, r["grad"], O.BF16, sc)
         assert _bits_equal(c["h_states_t"].numpy(), np.concatenate([mst, mm, vv]))
     pipe.close()
+
+
+def test_pipeline_resident_states_host_grads_device_param_copy(cuda_dev):
+    """The e2e configuration of bench.py (and its N>1 form): states in HBM,
+    bf16 grads read from pinned host memory, params written back over the
+    grads in host memory AND kept on the device (chunk.d_param, the rank's
+    slice of the full-param buffer that the all-gather then fills)."""
+    from paper_2403_06504_b200 import optim as F
+    sizes = [1 << 20, 4099, (1 << 18) + 8]
+    chunks, ref = _make_chunks(sizes, 11, cuda_dev, grads_on_host=True)
+    d_states = [c["h_states_t"].to(cuda_dev) for c in chunks]
+    d_params = [torch.zeros(c["n"], dtype=torch.bfloat16, device=cuda_dev) for c in chunks]
+    pipe = F.ChunkPipeline(max(sizes), slots=3, grads_on_host=True, params_to_host=True,
+                           keep_params_on_device=True, states_on_device=True)
+    desc = [dict(n=c["n"], h_states=s.data_ptr(), grad=c["grad_t"].data_ptr(),
+                 h_param=c["grad_t"].data_ptr(), d_param=p.data_ptr())
+            for c, s, p in zip(chunks, d_states, d_params)]
+    pipe.step(desc, F.Hparams(step=10))
+    pipe.wait()
+    sc = O.scalars(step=10)
+    for c, s, p, r in zip(chunks, d_states, d_params, ref):
+        n = r["grad"].size
+        st = r["states"]
+        mst, mm, vv = st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()
+        op = np.zeros(n, np.uint16)
+        O.adamw_step(mst, mm, vv, r["grad"], O.BF16, sc, param_out=op)
+        assert _bits_equal(s.cpu().numpy(), np.concatenate([mst, mm, vv]))
+        assert np.array_equal(p.cpu().view(torch.int16).numpy().view(np.uint16), op)
+        assert np.array_equal(c["grad_t"].view(torch.int16).numpy().view(np.uint16), op)
+    pipe.close()
