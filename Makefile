@@ -21,7 +21,7 @@ CUDA_OBJ := $(patsubst $(PKG)/csrc/cuda/%.cu,$(OBJDIR)/cuda/%.o,$(CUDA_SRC))
 HDRS     := $(wildcard include/offsim/*.hpp include/offsim/*.h include/fuyou/*.h) \
             $(wildcard $(PKG)/csrc/core/*.hpp $(PKG)/csrc/cuda/*.cuh)
 
-all: $(LIBDIR)/liboffsim.so $(if $(CORE_SRC),build/offsim_dump build/io_engine_test build/offsim) oracle
+all: $(LIBDIR)/liboffsim.so $(if $(CORE_SRC),build/offsim_dump build/io_engine_test build/offsim build/graph_dump) oracle
 
 $(OBJDIR)/core/%.o: $(PKG)/csrc/core/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
@@ -51,6 +51,10 @@ build/offsim_dump: tests/parity/offsim_dump.cpp build/liboffsim_core.a
 build/offsim: tools/offsim_main.cpp $(LIBDIR)/liboffsim.so
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) $< -L$(LIBDIR) -l:liboffsim.so.0 -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)' -o $@
+
+# mapped task graph (what offsim::execute runs) as JSON, for scripts/critical_path.py
+build/graph_dump: tools/graph_dump.cpp build/liboffsim_core.a
+	$(CXX) $(CXXFLAGS) $< build/liboffsim_core.a -pthread -o $@
 
 build/io_engine_test: tests/parity/io_engine_test.cpp $(PKG)/csrc/core/io_engine.cpp $(PKG)/csrc/core/io_engine.hpp
 	@mkdir -p build

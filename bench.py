@@ -659,6 +659,9 @@ def iteration_phase(F):
                     "executed_makespan_s": d["executed"]["makespan_s"],
                     "planned_makespan_s": d["planned"]["makespan_s"],
                     "executed_over_planned": d["executed"]["makespan_s"] / d["planned"]["makespan_s"],
+                    "predicted_makespan_s": d["predicted"]["makespan_s"],
+                    "executed_over_predicted": d["executed_over_predicted"],
+                    "effective_link_gbs": d["hw_predicted"]["bw_gpu"] / 1e9,
                     "tasks": d["task_count"], "swap_checks": d["swap_checks"],
                     "swap_mismatches": d["swap_mismatches"],
                     "optimizer_kernel_params_per_s": d["optimizer"]["kernel_params_per_s"],

@@ -148,17 +148,32 @@ struct MeasuredRates {
     double file_write_bps = 0.0;
     double optimizer_params_per_s = 0.0;
     double compute_flops = 0.0;
+    double compute_headroom = 1.0;  // compute_flops = measured x this (gemm mode)
     std::uint64_t gpu_mem = 0;
     std::uint64_t cpu_mem = 0;
+    // Delivered link rates when this graph's own host<->device copies run
+    // back to back on both lanes at once (duplex, real copy sizes): what an
+    // overlapped schedule actually gets from PCIe, vs the simplex burst
+    // rates above.
+    double h2d_effective_bps = 0.0;
+    double d2h_effective_bps = 0.0;
 };
+// Upper-bound rates (burst x 1.05): the issue order and the unchanged
+// roofline-lower-bound invariant on the real trace.
 HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRates& r);
+// Effective rates (duplex link, measured kernel / compute, no headroom): the
+// reference's DES on these predicts the executed makespan (SURVEY §8f
+// rank 3: analytic vs executed).
+HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const MeasuredRates& r);
 
 struct ExecReport {
     TaskGraph graph;        // the mapped graph that ran
     SimTrace trace;         // real timings (CUDA events), same type as simulate()
     SimTrace planned;       // simulate() of the mapped graph on `hw_exec`
+    SimTrace predicted;     // simulate() of the mapped graph on `hw_predicted`
     InvariantReport invariants;
     HardwareConfig hw_exec;
+    HardwareConfig hw_predicted;
     std::map<std::string, double> reference_bytes; // "<lane>/<payload>" of the input graph
     std::map<std::string, double> physical_bytes;  // "h2d|d2h|file_read|file_write/<payload>"
     double grad_sq_sum = 0.0;

@@ -150,6 +150,8 @@ std::string exec_summary_json(const ExecReport& r) {
     for (const auto& e : r.invariants.entries)
         checks.push_back(json{{"name", e.name}, {"pass", e.pass}, {"detail", e.detail}});
     const HardwareConfig& h = r.hw_exec;
+    const HardwareConfig& e = r.hw_predicted;
+    const double pred_s = static_cast<double>(r.predicted.makespan_ns) * 1e-9;
     const json doc = {
         {"schema_version", 1},
         {"command", "execute"},
@@ -161,6 +163,11 @@ std::string exec_summary_json(const ExecReport& r) {
                          {"gpu_mem", h.gpu_mem}, {"cpu_mem", h.cpu_mem}}},
         {"executed", trace_stats(r.trace)},
         {"planned", trace_stats(r.planned)},
+        {"hw_predicted", json{{"bw_gpu", e.bw_gpu}, {"bw_s2c", e.bw_s2c}, {"bw_c2s", e.bw_c2s},
+                              {"cpu_opt_tput", e.cpu_opt_tput}, {"gpu_tput", e.gpu_tput}}},
+        {"predicted", trace_stats(r.predicted)},
+        {"executed_over_predicted",
+         pred_s > 0 ? static_cast<double>(r.trace.makespan_ns) * 1e-9 / pred_s : 0.0},
         {"optimizer", optimizer_json(r)},
         {"reference_bytes", bytes_json(r.reference_bytes)},
         {"physical_bytes", bytes_json(r.physical_bytes)},

@@ -279,4 +279,19 @@ HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRat
     return hw;
 }
 
+HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const MeasuredRates& r) {
+    HardwareConfig hw = b200_hardware(planned_on, r);
+    hw.name = "b200-effective";
+    // one bw_gpu serves both link lanes in the reference's model
+    // (simulator.cpp:17-35): take the slower delivered direction
+    const double eff = std::min(r.h2d_effective_bps > 0 ? r.h2d_effective_bps : r.h2d_bps,
+                                r.d2h_effective_bps > 0 ? r.d2h_effective_bps : r.d2h_bps);
+    hw.bw_gpu = eff;
+    if (r.file_read_bps > 0) hw.bw_s2c = r.file_read_bps;
+    if (r.file_write_bps > 0) hw.bw_c2s = r.file_write_bps;
+    hw.cpu_opt_tput = r.optimizer_params_per_s;
+    hw.gpu_tput = r.compute_flops / r.compute_headroom;
+    return hw;
+}
+
 } // namespace offsim

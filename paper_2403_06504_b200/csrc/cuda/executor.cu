@@ -469,8 +469,11 @@ void Engine::setup() {
         gemm_b_ = Device(2 * bc_elems);
         gemm_c_ = Device(2 * bc_elems);
         gemm_ws_ = Device(32ull << 20);
-        check_cuda(cudaMemset(gemm_a_.p, 0, 2 * a_elems), "memset");
-        check_cuda(cudaMemset(gemm_b_.p, 0, 2 * bc_elems), "memset");
+        // random bf16 operands (~1e-3): zero operands would understate the
+        // tensor cores' power draw and so overstate the rate beside the optimizer
+        fill_grads<<<592, 256>>>(static_cast<std::uint16_t*>(gemm_a_.p), a_elems, 3);
+        fill_grads<<<592, 256>>>(static_cast<std::uint16_t*>(gemm_b_.p), bc_elems, 4);
+        check_cuda(cudaGetLastError(), "fill gemm operands");
         if (cublasCreate(&blas_) != CUBLAS_STATUS_SUCCESS) throw fy::DeviceError("cublasCreate failed");
         cublasSetStream(blas_, lane_stream(ResourceId::gpu_compute));
         cublasSetWorkspace(blas_, gemm_ws_.p, 32ull << 20);
@@ -569,6 +572,54 @@ MeasuredRates Engine::calibrate() {
     r.d2h_bps = bytes / timed(lane_stream(ResourceId::link_g2c), [&](cudaStream_t s) {
                     check_cuda(cudaMemcpyAsync(h.p, slot, bytes, cudaMemcpyDeviceToHost, s), "d2h");
                 });
+    // Effective duplex rates: replay this graph's own copy sizes (capped at
+    // 256 MiB each, 2 GiB per direction, in task order) back to back on both
+    // link lanes at once — small copies and duplex contention included.
+    {
+        constexpr std::uint64_t kEach = 256ull << 20, kTotal = 2ull << 30;
+        std::vector<std::uint64_t> up, down;
+        std::uint64_t up_b = 0, down_b = 0, biggest = 0;
+        for (const Task& t : g_.tasks) {
+            if (t.kind != TaskKind::transfer || t.work <= 0.0) continue;
+            const std::uint64_t b = std::min<std::uint64_t>(static_cast<std::uint64_t>(t.work), kEach);
+            if (t.resource == ResourceId::link_c2g && up_b < kTotal) { up.push_back(b); up_b += b; }
+            if (t.resource == ResourceId::link_g2c && down_b < kTotal) { down.push_back(b); down_b += b; }
+            if ((t.resource == ResourceId::link_c2g || t.resource == ResourceId::link_g2c))
+                biggest = std::max(biggest, b);
+        }
+        if (!up.empty() || !down.empty()) {
+            Pinned hu(biggest), hd(biggest);
+            Device du(biggest), dd(biggest);
+            cudaStream_t su = lane_stream(ResourceId::link_c2g), sd = lane_stream(ResourceId::link_g2c);
+            cudaEvent_t go, eu, ed;
+            check_cuda(cudaEventCreate(&go), "event");
+            check_cuda(cudaEventCreate(&eu), "event");
+            check_cuda(cudaEventCreate(&ed), "event");
+            double best_u = 1e30, best_d = 1e30;
+            for (int it = 0; it < 2; ++it) {
+                check_cuda(cudaDeviceSynchronize(), "sync");
+                check_cuda(cudaEventRecord(go, su), "record");
+                check_cuda(cudaStreamWaitEvent(sd, go, 0), "wait");
+                for (const std::uint64_t b : up)
+                    check_cuda(cudaMemcpyAsync(du.p, hu.p, b, cudaMemcpyHostToDevice, su), "h2d");
+                for (const std::uint64_t b : down)
+                    check_cuda(cudaMemcpyAsync(hd.p, dd.p, b, cudaMemcpyDeviceToHost, sd), "d2h");
+                check_cuda(cudaEventRecord(eu, su), "record");
+                check_cuda(cudaEventRecord(ed, sd), "record");
+                check_cuda(cudaDeviceSynchronize(), "sync");
+                float mu = 0, md = 0;
+                check_cuda(cudaEventElapsedTime(&mu, go, eu), "elapsed");
+                check_cuda(cudaEventElapsedTime(&md, go, ed), "elapsed");
+                best_u = std::min(best_u, mu * 1e-3);
+                best_d = std::min(best_d, md * 1e-3);
+            }
+            if (up_b > 0) r.h2d_effective_bps = up_b / best_u;
+            if (down_b > 0) r.d2h_effective_bps = down_b / best_d;
+            cudaEventDestroy(go);
+            cudaEventDestroy(eu);
+            cudaEventDestroy(ed);
+        }
+    }
     // fused kernel rate on a scratch copy (does not touch the real states)
     r.optimizer_params_per_s = 1e12; // no optimizer task: the lane stays empty
     if (has_update_) {
@@ -625,7 +676,8 @@ MeasuredRates Engine::calibrate() {
         const int h = static_cast<int>(model_.hidden_dim);
         const double sec = timed(lane_stream(ResourceId::gpu_compute),
                                  [&](cudaStream_t s) { gemm(s, tokens, 4 * h, h); });
-        r.compute_flops = 2.0 * tokens * 4.0 * h * h / sec * 1.05;  // upper bound
+        r.compute_headroom = 1.05;
+        r.compute_flops = 2.0 * tokens * 4.0 * h * h / sec * r.compute_headroom;  // upper bound
     }
     std::size_t free_b = 0, total_b = 0;
     check_cuda(cudaMemGetInfo(&free_b, &total_b), "meminfo");
@@ -935,6 +987,8 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
     if (rates.compute_flops <= 0) rates.compute_flops = hw.gpu_tput;
     rep.hw_exec = b200_hardware(hw, rates);
     rep.planned = simulate(rep.graph, rep.hw_exec);
+    rep.hw_predicted = b200_hardware_effective(hw, rates);
+    rep.predicted = simulate(rep.graph, rep.hw_predicted);
     eng.run(rep.planned, rep);
     rep.invariants = check_trace_invariants(rep.graph, rep.trace, rep.hw_exec);
     return rep;

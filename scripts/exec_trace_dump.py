@@ -1,0 +1,26 @@
+#!/usr/bin/env python
+"""Dump executed traces (offsim_execute) + summaries for offline analysis of
+executed vs planned makespan. Writes gpurun_out/exec_<tag>_{summary,trace}.json."""
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+import exec_api as X  # noqa: E402
+
+out = ROOT / "gpurun_out"
+out.mkdir(exist_ok=True)
+cases = {
+    "c1_b8": (X.scenario(batch=8), {"tier": "host", "compute_rate": 1.4e15}),
+    "c1_b128": (X.scenario(batch=128), {"tier": "host", "compute_rate": 1.4e15}),
+    "13b_4blk": (X.scenario(layers=4, heads=40, hidden=5120, batch=8, name="13b4"),
+                 {"tier": "host", "compute_mode": "gemm"}),
+}
+for tag in (sys.argv[1:] or list(cases)):
+    sc, opts = cases[tag]
+    st, summ, trace, err = X.execute(sc, opts, want_trace=True)
+    (out / f"exec_{tag}_summary.json").write_text(json.dumps(summ, indent=1))
+    (out / f"exec_{tag}_trace.json").write_text(trace or "")
+    print(tag, st, err, summ["executed"]["makespan_s"], summ["planned"]["makespan_s"])
