@@ -18,8 +18,16 @@ cases = {
     "13b_4blk": (X.scenario(layers=4, heads=40, hidden=5120, batch=8, name="13b4"),
                  {"tier": "host", "compute_mode": "gemm"}),
 }
-for tag in (sys.argv[1:] or list(cases)):
+# args: [tag ...] [--opts JSON] (extra ExecOptions merged into every case)
+args = sys.argv[1:]
+extra = {}
+if "--opts" in args:
+    i = args.index("--opts")
+    extra = json.loads(args[i + 1])
+    del args[i:i + 2]
+for tag in (args or list(cases)):
     sc, opts = cases[tag]
+    opts = {**opts, **extra}
     st, summ, trace, err = X.execute(sc, opts, want_trace=True)
     (out / f"exec_{tag}_summary.json").write_text(json.dumps(summ, indent=1))
     (out / f"exec_{tag}_trace.json").write_text(trace or "")
