@@ -885,6 +885,9 @@ def main():
     pcie = None
     if rank == 0 and world == 1:
         pcie = pcie_peaks(torch)
+        node = C.c_int(-1)
+        F.check(F.LIB.fy_device_numa_node(local, C.byref(node)))
+        pcie["gpu_numa_node"] = node.value  # fy_host_alloc places the host tier there
         extra["pcie"] = pcie
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

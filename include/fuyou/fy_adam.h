@@ -213,9 +213,19 @@ fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32
 fy_status fy_graph_execute(const char* scenario_json, const char* exec_opts_json,
                            const fy_chunk* chunks, uint32_t chunk_count, char** summary_json_out);
 
-/* Pinned host allocation helpers (cudaHostAlloc, portable). */
+/* Pinned host allocation (page-locked, portable) on the NUMA node of the
+ * GPU that will stream it — the host tier's "NUMA-local pinned memory"
+ * (SURVEY.md §8e). fy_host_alloc: the current device's node (PCI sysfs).
+ * fy_host_alloc_on: numa_node >= 0 prefers that node, -1 the current
+ * device's node, -2 no placement policy. Falls back to cudaHostAlloc when
+ * registration is refused. Free either with fy_host_free. */
 fy_status fy_host_alloc(uint64_t bytes, void** out);
+fy_status fy_host_alloc_on(uint64_t bytes, int numa_node, void** out);
 fy_status fy_host_free(void* p);
+/* NUMA node of a GPU (-1 if the platform does not report one) and of the
+ * page holding p (< 0 if unknown). */
+fy_status fy_device_numa_node(int device, int* node);
+fy_status fy_host_numa_node(const void* p, int* node);
 
 #ifdef __cplusplus
 } /* extern "C" */

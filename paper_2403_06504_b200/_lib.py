@@ -99,6 +99,9 @@ def _load() -> C.CDLL:
                                      C.POINTER(C.c_uint64)]),
         "fy_host_alloc": (st, [C.c_uint64, C.POINTER(C.c_void_p)]),
         "fy_host_free": (st, [C.c_void_p]),
+        "fy_host_alloc_on": (st, [C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]),
+        "fy_device_numa_node": (st, [C.c_int, C.POINTER(C.c_int)]),
+        "fy_host_numa_node": (st, [C.c_void_p, C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

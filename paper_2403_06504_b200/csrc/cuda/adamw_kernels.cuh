@@ -74,4 +74,15 @@ Geometry geometry(int device);
 // stages (3 or 6).
 void set_tuning(int path, int unroll, int ctas_per_sm);
 
+// NUMA-local pinned host memory (host_mem.cu). device_numa_node: the GPU's
+// node from PCI sysfs (-1 unknown). host_alloc: page-locked, portable,
+// preferring `node` (-1: no policy); nullptr on failure; *placed = node of
+// the first page when a policy was applied, else -1. host_free: false if p
+// did not come from host_alloc. host_numa_node: node of p's page (<0 if
+// unknown / unpopulated).
+int device_numa_node(int device);
+void* host_alloc(std::uint64_t bytes, int node, int* placed);
+bool host_free(void* p);
+int host_numa_node(const void* p);
+
 } // namespace fy

@@ -175,8 +175,13 @@ struct Pinned {
     void* p = nullptr;
     Pinned() = default;
     explicit Pinned(std::uint64_t bytes) {
-        check_cuda(cudaHostAlloc(&p, std::max<std::uint64_t>(bytes, kAlign), cudaHostAllocPortable),
-                   "cudaHostAlloc (executor host buffers)");
+        // NUMA-local to the executing GPU (host_mem.cu); cudaHostAlloc if
+        // registration is refused
+        int dev = 0;
+        check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+        bytes = std::max<std::uint64_t>(bytes, kAlign);
+        p = fy::host_alloc(bytes, fy::device_numa_node(dev), nullptr);
+        if (!p) check_cuda(cudaHostAlloc(&p, bytes, cudaHostAllocPortable), "cudaHostAlloc (executor host buffers)");
     }
     Pinned(Pinned&& o) noexcept : p(o.p) { o.p = nullptr; }
     Pinned& operator=(Pinned&& o) noexcept {
@@ -184,7 +189,7 @@ struct Pinned {
         return *this;
     }
     ~Pinned() {
-        if (p) cudaFreeHost(p);
+        if (p && !fy::host_free(p)) cudaFreeHost(p);
     }
 };
 

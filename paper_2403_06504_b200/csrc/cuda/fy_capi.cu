@@ -206,25 +206,52 @@ fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32
     });
 }
 
-fy_status fy_host_alloc(uint64_t bytes, void** out) {
+fy_status fy_host_alloc_on(uint64_t bytes, int numa_node, void** out) {
     if (!out) return fail(FY_ERR_CONFIG, "null argument");
+    if (numa_node < -2) return fail(FY_ERR_CONFIG, "numa_node must be >= -2");
     return guard([&] {
-        void* p = nullptr;
-        const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
-        if (e == cudaErrorMemoryAllocation)
-            return fail(FY_ERR_INFEASIBLE, "pinned host allocation of " + std::to_string(bytes) +
-                                               " bytes failed");
-        fy::check_cuda(e, "cudaHostAlloc");
+        int node = numa_node;
+        if (node == -1) {
+            int dev = 0;
+            fy::check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+            node = fy::device_numa_node(dev);
+        }
+        void* p = fy::host_alloc(bytes, node == -2 ? -1 : node, nullptr);
+        if (!p) {
+            // registration refused (e.g. locked-memory limits): plain
+            // cudaHostAlloc, still page-locked, first-touch placement
+            const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+            if (e == cudaErrorMemoryAllocation)
+                return fail(FY_ERR_INFEASIBLE, "pinned host allocation of " + std::to_string(bytes) +
+                                                   " bytes failed");
+            fy::check_cuda(e, "cudaHostAlloc");
+        }
         *out = p;
         return FY_OK;
     });
 }
 
+fy_status fy_host_alloc(uint64_t bytes, void** out) { return fy_host_alloc_on(bytes, -1, out); }
+
 fy_status fy_host_free(void* p) {
     return guard([&] {
-        if (p) fy::check_cuda(cudaFreeHost(p), "cudaFreeHost");
+        if (p && !fy::host_free(p)) fy::check_cuda(cudaFreeHost(p), "cudaFreeHost");
         return FY_OK;
     });
+}
+
+fy_status fy_device_numa_node(int device, int* node) {
+    if (!node) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        *node = fy::device_numa_node(device);
+        return FY_OK;
+    });
+}
+
+fy_status fy_host_numa_node(const void* p, int* node) {
+    if (!p || !node) return fail(FY_ERR_CONFIG, "null argument");
+    *node = fy::host_numa_node(p);
+    return FY_OK;
 }
 
 } // extern "C"

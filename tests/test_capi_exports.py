@@ -103,6 +103,10 @@ def test_argument_validation_without_gpu():
     assert LIB.fy_pipeline_step(None, None, 0, None, 0) == FY_ERR_CONFIG
     assert LIB.fy_pipeline_wait(None, None, None) == FY_ERR_CONFIG
     assert LIB.fy_host_alloc(16, None) == FY_ERR_CONFIG
+    out = C.c_void_p()
+    assert LIB.fy_host_alloc_on(16, -3, C.byref(out)) == FY_ERR_CONFIG
+    assert LIB.fy_device_numa_node(0, None) == FY_ERR_CONFIG
+    assert LIB.fy_host_numa_node(None, None) == FY_ERR_CONFIG
 
 
 def test_graph_execute_rejects_bad_input_without_gpu():

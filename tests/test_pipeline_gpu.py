@@ -155,3 +155,32 @@ def test_pipeline_resident_states_host_grads_device_param_copy(cuda_dev):
         assert np.array_equal(p.cpu().view(torch.int16).numpy().view(np.uint16), op)
         assert np.array_equal(c["grad_t"].view(torch.int16).numpy().view(np.uint16), op)
     pipe.close()
+
+
+def test_numa_local_pinned_host_memory(cuda_dev):
+    """fy_host_alloc places the host tier on the GPU's NUMA node (PCI sysfs)
+    and page-locks it: the pages report that node (move_pages) when the
+    platform has one, and copies to / from it are page-locked DMA (the
+    pipeline's bit-exact results above run on these buffers)."""
+    import ctypes as C
+    from paper_2403_06504_b200._lib import LIB, check
+    node = C.c_int()
+    check(LIB.fy_device_numa_node(0, C.byref(node)))
+    p = C.c_void_p()
+    n = 64 << 20
+    check(LIB.fy_host_alloc(n, C.byref(p)))
+    try:
+        got = C.c_int()
+        check(LIB.fy_host_numa_node(p, C.byref(got)))
+        if node.value >= 0:
+            assert got.value == node.value
+        host = torch.frombuffer((C.c_uint8 * n).from_address(p.value), dtype=torch.uint8)
+        host[:] = 7
+        d = host.to(cuda_dev, non_blocking=True)
+        torch.cuda.synchronize()
+        assert int(d.sum().item()) == 7 * n
+    finally:
+        check(LIB.fy_host_free(p))
+    q = C.c_void_p()
+    check(LIB.fy_host_alloc_on(1 << 20, -2, C.byref(q)))  # no placement policy
+    check(LIB.fy_host_free(q))
