@@ -49,32 +49,39 @@ ChunkPipeline::ChunkPipeline(const fy_pipeline_config& cfg) : cfg_(cfg) {
     grad_bytes_ = dtype_bytes(cfg_.grad_dtype);
     param_bytes_ = dtype_bytes(cfg_.param_dtype);
 
-    check_cuda(cudaSetDevice(cfg_.device), "cudaSetDevice");
-    int lo = 0, hi = 0;
-    check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
-    check_cuda(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "h2d stream");
-    check_cuda(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "d2h stream");
-    // The update kernel is short next to the copies; give it the higher
-    // priority so it is not queued behind a synthetic backward.
-    check_cuda(cudaStreamCreateWithPriority(&opt_, cudaStreamNonBlocking, hi), "opt stream");
+    try {
+        check_cuda(cudaSetDevice(cfg_.device), "cudaSetDevice");
+        int lo = 0, hi = 0;
+        check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+        check_cuda(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "h2d stream");
+        check_cuda(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "d2h stream");
+        // The update kernel is short next to the copies; give it the higher
+        // priority so it is not queued behind a synthetic backward.
+        check_cuda(cudaStreamCreateWithPriority(&opt_, cudaStreamNonBlocking, hi), "opt stream");
 
-    const std::uint64_t n = cfg_.max_chunk_elems;
-    slots_.resize(cfg_.slots);
-    for (Slot& s : slots_) {
-        if (!cfg_.states_on_device) check_cuda(cudaMalloc(&s.states, 12ull * n), "slot states");
-        if (cfg_.grads_on_host) check_cuda(cudaMalloc(&s.grad, grad_bytes_ * n), "slot grad");
-        if (cfg_.params_to_host) check_cuda(cudaMalloc(&s.param, param_bytes_ * n), "slot param");
+        const std::uint64_t n = cfg_.max_chunk_elems;
+        slots_.resize(cfg_.slots);
+        for (Slot& s : slots_) {
+            if (!cfg_.states_on_device) check_cuda(cudaMalloc(&s.states, 12ull * n), "slot states");
+            if (cfg_.grads_on_host) check_cuda(cudaMalloc(&s.grad, grad_bytes_ * n), "slot grad");
+            if (cfg_.params_to_host) check_cuda(cudaMalloc(&s.param, param_bytes_ * n), "slot param");
+        }
+        check_cuda(cudaMalloc(&workspace_, sizeof(float) * kWorkspaceFloats), "workspace");
+        check_cuda(cudaMalloc(&d_norm_, sizeof(double)), "norm");
+        check_cuda(cudaMalloc(&d_nonfinite_, sizeof(int)), "nonfinite");
+        check_cuda(cudaHostAlloc(&h_norm_, sizeof(double), cudaHostAllocDefault), "h norm");
+        check_cuda(cudaHostAlloc(&h_nonfinite_, sizeof(int), cudaHostAllocDefault), "h nonfinite");
+        check_cuda(cudaEventCreate(&step_start_), "event");
+        check_cuda(cudaEventCreate(&step_end_), "event");
+    } catch (...) {
+        release();  // a failed allocation must not leak the earlier ones
+        throw;
     }
-    check_cuda(cudaMalloc(&workspace_, sizeof(float) * kWorkspaceFloats), "workspace");
-    check_cuda(cudaMalloc(&d_norm_, sizeof(double)), "norm");
-    check_cuda(cudaMalloc(&d_nonfinite_, sizeof(int)), "nonfinite");
-    check_cuda(cudaHostAlloc(&h_norm_, sizeof(double), cudaHostAllocDefault), "h norm");
-    check_cuda(cudaHostAlloc(&h_nonfinite_, sizeof(int), cudaHostAllocDefault), "h nonfinite");
-    check_cuda(cudaEventCreate(&step_start_), "event");
-    check_cuda(cudaEventCreate(&step_end_), "event");
 }
 
-ChunkPipeline::~ChunkPipeline() {
+ChunkPipeline::~ChunkPipeline() { release(); }
+
+void ChunkPipeline::release() noexcept {
     cudaSetDevice(cfg_.device);
     if (pending_) cudaEventSynchronize(step_end_);
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
@@ -93,6 +100,16 @@ ChunkPipeline::~ChunkPipeline() {
     if (h2d_) cudaStreamDestroy(h2d_);
     if (d2h_) cudaStreamDestroy(d2h_);
     if (opt_) cudaStreamDestroy(opt_);
+    events_.clear();
+    slots_.clear();
+    step_start_ = step_end_ = nullptr;
+    workspace_ = nullptr;
+    d_norm_ = nullptr;
+    d_nonfinite_ = nullptr;
+    h_norm_ = nullptr;
+    h_nonfinite_ = nullptr;
+    h2d_ = d2h_ = opt_ = nullptr;
+    pending_ = false;
 }
 
 void ChunkPipeline::ensure_events(std::uint32_t count) {

@@ -35,6 +35,7 @@ class ChunkPipeline {
 public:
     explicit ChunkPipeline(const fy_pipeline_config& cfg);
     ~ChunkPipeline();
+    void release() noexcept;  // frees everything allocated so far (dtor, failed ctor)
     ChunkPipeline(const ChunkPipeline&) = delete;
     ChunkPipeline& operator=(const ChunkPipeline&) = delete;
 
