@@ -97,10 +97,11 @@ std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint
     auto* cqes = static_cast<io_uring_cqe*>(cqes_);
     std::vector<std::uint64_t> short_pieces;
     std::uint64_t next = 0, inflight = 0, failed_errno = 0;
-    while (next < pieces || inflight > 0) {
+    unsigned unsubmitted = 0; // SQEs past the tail the kernel has not consumed yet
+    while (next < pieces || inflight > 0 || unsubmitted > 0) {
         unsigned queued = 0;
         unsigned tail = __atomic_load_n(sq_tail_, __ATOMIC_RELAXED);
-        while (next < pieces && inflight + queued < depth_) {
+        while (next < pieces && inflight + unsubmitted + queued < depth_) {
             const std::uint64_t off = next * piece_;
             const unsigned idx = tail & *sq_mask_;
             io_uring_sqe& e = sqes[idx];
@@ -117,9 +118,16 @@ std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint
             ++next;
         }
         __atomic_store_n(sq_tail_, tail, __ATOMIC_RELEASE);
-        const int r = uring_enter(ring_fd_, queued, 1, IORING_ENTER_GETEVENTS);
-        if (r < 0 && errno != EINTR) return std::string("io_uring_enter failed: ") + std::strerror(errno);
-        inflight += queued;
+        unsubmitted += queued;
+        // consumed SQEs become in flight; a partial submit (or EINTR) leaves
+        // the rest in the ring for the next enter
+        const int r = uring_enter(ring_fd_, unsubmitted, inflight + unsubmitted > 0 ? 1 : 0,
+                                  IORING_ENTER_GETEVENTS);
+        if (r < 0 && errno != EINTR && errno != EAGAIN && errno != EBUSY)
+            return std::string("io_uring_enter failed: ") + std::strerror(errno);
+        const unsigned consumed = r > 0 ? std::min<unsigned>(static_cast<unsigned>(r), unsubmitted) : 0;
+        unsubmitted -= consumed;
+        inflight += consumed;
         unsigned head = __atomic_load_n(cq_head_, __ATOMIC_RELAXED);
         const unsigned ctail = __atomic_load_n(cq_tail_, __ATOMIC_ACQUIRE);
         while (head != ctail) {
