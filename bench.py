@@ -769,6 +769,9 @@ def ssd_tier_phase(F, blocks=8, ring=3):
             "pinned_host_bytes": d["pinned_host_bytes"], "file_bytes": file_bytes,
             "file_lane_gbs": file_bytes / ssd_busy / 1e9 if ssd_busy else None,
             "makespan_s": d["executed"]["makespan_s"], "planned_s": d["planned"]["makespan_s"],
+            "predicted_s": d["predicted"]["makespan_s"],
+            "executed_over_predicted": d["executed_over_predicted"],
+            "hw_predicted": d["hw_predicted"],
             "io_engine": d["io_engine"], "all_invariants_pass": d["all_invariants_pass"],
             "optimizer_kernel_params_per_s": d["optimizer"]["kernel_params_per_s"]}
 

@@ -157,6 +157,9 @@ struct MeasuredRates {
     // rates above.
     double h2d_effective_bps = 0.0;
     double d2h_effective_bps = 0.0;
+    // file tier: this graph's own file-lane operations replayed in task order
+    double file_read_effective_bps = 0.0;
+    double file_write_effective_bps = 0.0;
 };
 // Upper-bound rates (burst x 1.05): the issue order and the unchanged
 // roofline-lower-bound invariant on the real trace.

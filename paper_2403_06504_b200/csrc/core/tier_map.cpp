@@ -287,8 +287,10 @@ HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const M
     const double eff = std::min(r.h2d_effective_bps > 0 ? r.h2d_effective_bps : r.h2d_bps,
                                 r.d2h_effective_bps > 0 ? r.d2h_effective_bps : r.d2h_bps);
     hw.bw_gpu = eff;
-    if (r.file_read_bps > 0) hw.bw_s2c = r.file_read_bps;
-    if (r.file_write_bps > 0) hw.bw_c2s = r.file_write_bps;
+    if (r.file_read_bps > 0)
+        hw.bw_s2c = r.file_read_effective_bps > 0 ? r.file_read_effective_bps : r.file_read_bps;
+    if (r.file_write_bps > 0)
+        hw.bw_c2s = r.file_write_effective_bps > 0 ? r.file_write_effective_bps : r.file_write_bps;
     hw.cpu_opt_tput = r.optimizer_params_per_s;
     hw.gpu_tput = r.compute_flops / r.compute_headroom;
     return hw;

@@ -672,6 +672,25 @@ MeasuredRates Engine::calibrate() {
         }
         r.file_write_bps = bytes / best_w;
         r.file_read_bps = bytes / best_r;
+        // effective: replay the graph's own file-lane operations in task
+        // order (each <= the probe size, <= 2 GiB in total) — reads and
+        // writes interleaved as the iteration issues them
+        double rd_b = 0, rd_s = 0, wr_b = 0, wr_s = 0;
+        for (const Task& t : g_.tasks) {
+            if (t.resource != ResourceId::link_ssd || t.work <= 0.0) continue;
+            if (rd_b + wr_b >= double(2ull << 30)) break;
+            const std::uint64_t b = round_up(std::min<std::uint64_t>(static_cast<std::uint64_t>(t.work), bytes));
+            IoRequest op = w;
+            op.bytes = b;
+            op.write = t.dir == TransferDir::c2s;
+            const auto t0 = std::chrono::steady_clock::now();
+            run_io(&op);
+            const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            (op.write ? wr_b : rd_b) += static_cast<double>(b);
+            (op.write ? wr_s : rd_s) += sec;
+        }
+        if (rd_s > 0) r.file_read_effective_bps = rd_b / rd_s;
+        if (wr_s > 0) r.file_write_effective_bps = wr_b / wr_s;
         if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
     }
     r.compute_flops = opt_.compute_rate > 0 ? opt_.compute_rate : 0.0;
