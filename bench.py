@@ -57,6 +57,7 @@ METRIC = "Adam params/sec & GB/s vs HBM/host-link roofline at 1/2/4/8 B200"
 UNIT = "params/s"
 BYTES_RESIDENT = 28  # 2 grad r + 12 state r + 12 state w + 2 param w
 SEED = 20240817
+E2E_PIECES = 4  # pipeline units per block in the e2e path
 
 
 def shape(layers: int, hidden: int):
@@ -584,11 +585,18 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
     # the chunk's full-param buffer on the device, and an in-place NCCL
     # all-gather assembles the rest (no extra host round trip)
     rank = dist.get_rank() if world > 1 else 0
-    pipe = F.optim.ChunkPipeline(n, slots=3, grads_on_host=True, params_to_host=True,
-                                 keep_params_on_device=world > 1, states_on_device=True)
-    chunks = [dict(n=n, h_states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value,
-                   d_param=full[k][rank * n:(rank + 1) * n].data_ptr() if world > 1 else None)
-              for k in range(L)]
+    # each block is fed to the pipeline as E2E_PIECES units (8-aligned; the
+    # SoA states stay where they are, fy_chunk.states_stride = slice), so the
+    # copy engines fill and drain at piece granularity
+    bounds = [min(n, (n * q // E2E_PIECES + 7) // 8 * 8) for q in range(E2E_PIECES)] + [n]
+    spans = [(a, b) for a, b in zip(bounds, bounds[1:]) if b > a]
+    pipe = F.optim.ChunkPipeline(max(b - a for a, b in spans), slots=4, grads_on_host=True,
+                                 params_to_host=True, keep_params_on_device=world > 1,
+                                 states_on_device=True)
+    chunks = [dict(n=b - a, h_states=states[k].data_ptr() + 4 * a, states_stride=n,
+                   grad=hbuf[k].value + 2 * a, h_param=hbuf[k].value + 2 * a,
+                   d_param=full[k][rank * n + a:rank * n + b].data_ptr() if world > 1 else None)
+              for k in range(L) for a, b in spans]
     hp = F.optim.Hparams()
 
     def step(i):
@@ -621,7 +629,8 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
         "path": "fy_pipeline_step (C ABI): host bf16 grads H2D -> fused AdamW on HBM-resident "
                 "states -> bf16 params D2H into the same host buffer; wall clock"
                 + ("; + in-place NCCL all-gather of the device-side bf16 slices" if world > 1 else ""),
-        "launches": args.steps * L * 2,
+        "launches": args.steps * len(chunks) * 2,
+        "pieces_per_block": len(spans),
     }
 
 

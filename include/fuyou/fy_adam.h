@@ -177,6 +177,10 @@ typedef struct fy_chunk {
     void* h_param;        /* pinned host [n] params (params_to_host=1)      */
     void* d_param;        /* device [n] params (keep_params_on_device=1)    */
     void* grad_ready;     /* optional cudaEvent_t the update must wait on   */
+    uint64_t states_stride; /* elements from master to m and m to v in
+                               h_states (0 = n, i.e. contiguous [master|m|v]);
+                               > n lets a piece of a larger chunk's SoA
+                               arrays be one pipeline unit               */
 } fy_chunk;
 
 /* Per-chunk timings of the last step, in ns relative to the step start

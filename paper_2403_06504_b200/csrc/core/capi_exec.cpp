@@ -298,6 +298,9 @@ fy_status fy_graph_execute(const char* scenario_json, const char* exec_opts_json
             if (chunks[k].n != 12ull * sc.model.hidden_dim * sc.model.hidden_dim)
                 throw offsim::ConfigError("fy_graph_execute: chunk " + std::to_string(k) +
                                           " size differs from 12*h^2");
+            if (chunks[k].states_stride != 0 && chunks[k].states_stride != chunks[k].n)
+                throw offsim::ConfigError("fy_graph_execute: chunk " + std::to_string(k) +
+                                          ": strided states are a pipeline feature (contiguous here)");
             bufs.push_back({chunks[k].h_states, chunks[k].h_param, chunks[k].grad});
         }
         return offsim::run_exec(sc, exec_opts_json, chunk_count ? &bufs : nullptr, summary_json_out,

@@ -128,10 +128,17 @@ void ChunkPipeline::issue_h2d(std::uint32_t i) {
     if (i >= S) check_cuda(cudaStreamWaitEvent(h2d_, ev(i - S, kD2hEnd), 0), "wait slot");
     if (i >= 2) check_cuda(cudaStreamWaitEvent(h2d_, ev(i - 2, kUpdEnd), 0), "wait read gate");
     check_cuda(cudaEventRecord(ev(i, kH2dStart), h2d_), "record");
-    if (!cfg_.states_on_device)
-        check_cuda(cudaMemcpyAsync(slot.states, c.h_states, 12ull * c.n, cudaMemcpyHostToDevice,
-                                   h2d_),
-                   "H2D states");
+    if (!cfg_.states_on_device) {
+        const std::uint64_t stride = c.states_stride ? c.states_stride : c.n;
+        if (stride == c.n)
+            check_cuda(cudaMemcpyAsync(slot.states, c.h_states, 12ull * c.n, cudaMemcpyHostToDevice,
+                                       h2d_),
+                       "H2D states");
+        else  // master, m, v rows of a strided SoA -> contiguous slot
+            check_cuda(cudaMemcpy2DAsync(slot.states, 4 * c.n, c.h_states, 4 * stride, 4 * c.n, 3,
+                                         cudaMemcpyHostToDevice, h2d_),
+                       "H2D states (strided)");
+    }
     if (cfg_.grads_on_host)
         check_cuda(cudaMemcpyAsync(slot.grad, c.grad, std::uint64_t(grad_bytes_) * c.n,
                                    cudaMemcpyHostToDevice, h2d_),
@@ -149,9 +156,11 @@ void ChunkPipeline::issue_update(std::uint32_t i) {
     check_cuda(cudaEventRecord(ev(i, kUpdStart), opt_), "record");
     AdamLaunch a{};
     float* states = reinterpret_cast<float*>(cfg_.states_on_device ? c.h_states : slot.states);
+    // staged slots are contiguous; device-resident states keep the caller's stride
+    const std::uint64_t stride = cfg_.states_on_device && c.states_stride ? c.states_stride : c.n;
     a.master = states;
-    a.m = states + c.n;
-    a.v = states + 2 * c.n;
+    a.m = states + stride;
+    a.v = states + 2 * stride;
     a.grad = cfg_.grads_on_host ? slot.grad : c.grad;
     a.grad_dtype = cfg_.grad_dtype;
     a.param = cfg_.keep_params_on_device ? c.d_param : (cfg_.params_to_host ? slot.param : nullptr);
@@ -171,10 +180,17 @@ void ChunkPipeline::issue_d2h(std::uint32_t i) {
     Slot& slot = slots_[i % slots_.size()];
     check_cuda(cudaStreamWaitEvent(d2h_, ev(i, kUpdEnd), 0), "wait update");
     check_cuda(cudaEventRecord(ev(i, kD2hStart), d2h_), "record");
-    if (!cfg_.states_on_device)
-        check_cuda(cudaMemcpyAsync(c.h_states, slot.states, 12ull * c.n, cudaMemcpyDeviceToHost,
-                                   d2h_),
-                   "D2H states");
+    if (!cfg_.states_on_device) {
+        const std::uint64_t stride = c.states_stride ? c.states_stride : c.n;
+        if (stride == c.n)
+            check_cuda(cudaMemcpyAsync(c.h_states, slot.states, 12ull * c.n, cudaMemcpyDeviceToHost,
+                                       d2h_),
+                       "D2H states");
+        else
+            check_cuda(cudaMemcpy2DAsync(c.h_states, 4 * stride, slot.states, 4 * c.n, 4 * c.n, 3,
+                                         cudaMemcpyDeviceToHost, d2h_),
+                       "D2H states (strided)");
+    }
     if (cfg_.params_to_host) {
         const void* src = cfg_.keep_params_on_device ? c.d_param : slot.param;
         check_cuda(cudaMemcpyAsync(c.h_param, src, std::uint64_t(param_bytes_) * c.n,
@@ -193,6 +209,8 @@ void ChunkPipeline::step(const fy_chunk* chunks, std::uint32_t count, const fy_a
         if (c.n == 0 || c.n > cfg_.max_chunk_elems)
             throw ArgError("pipeline: chunk " + std::to_string(i) + " size out of range");
         if (!c.h_states || !c.grad) throw ArgError("pipeline: chunk missing states or grad");
+        if (c.states_stride != 0 && c.states_stride < c.n)
+            throw ArgError("pipeline: chunk " + std::to_string(i) + " states_stride < n");
         if (cfg_.params_to_host && !c.h_param) throw ArgError("pipeline: chunk missing h_param");
         if (cfg_.keep_params_on_device && !c.d_param)
             throw ArgError("pipeline: chunk missing d_param");

@@ -184,3 +184,37 @@ def test_numa_local_pinned_host_memory(cuda_dev):
     q = C.c_void_p()
     check(LIB.fy_host_alloc_on(1 << 20, -2, C.byref(q)))  # no placement policy
     check(LIB.fy_host_free(q))
+
+
+@pytest.mark.parametrize("states_on_device", [False, True])
+def test_pipeline_strided_pieces_equal_whole_chunk(cuda_dev, states_on_device):
+    """fy_chunk.states_stride: one chunk's SoA [master | m | v] (stride n)
+    streamed as P pieces (each piece's master/m/v rows at stride n, 2D
+    copies for host states, strided kernel pointers for device states)
+    equals the oracle on the whole chunk. This is how the bench's e2e path
+    splits a 13B block into pipeline units without re-laying out HBM."""
+    from paper_2403_06504_b200 import optim as F
+    n, pieces = (1 << 20) + 24, 4
+    bounds = [0, 262144, 524296, 786440, n]  # 8-aligned, ragged last piece
+    chunks, ref = _make_chunks([n], 21, cuda_dev, grads_on_host=True)
+    c = chunks[0]
+    states = c["h_states_t"].to(cuda_dev) if states_on_device else c["h_states_t"]
+    pipe = F.ChunkPipeline(max(b - a for a, b in zip(bounds, bounds[1:])), slots=3,
+                           grads_on_host=True, params_to_host=True, states_on_device=states_on_device)
+    desc = [dict(n=b - a, h_states=states.data_ptr() + 4 * a, grad=c["grad_t"].data_ptr() + 2 * a,
+                 h_param=c["h_param_t"].data_ptr() + 2 * a, states_stride=n)
+            for a, b in zip(bounds, bounds[1:])]
+    assert len(desc) == pieces
+    pipe.step(desc, F.Hparams(step=10), want_grad_norm=True)
+    sq, bad = pipe.wait()
+    st = ref[0]["states"]
+    mst, mm, vv = st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()
+    op = np.zeros(n, np.uint16)
+    sq_ref, _ = O.adamw_step(mst, mm, vv, ref[0]["grad"], O.BF16, O.scalars(step=10), param_out=op)
+    got = states.cpu().numpy() if states_on_device else states.numpy()
+    assert _bits_equal(got, np.concatenate([mst, mm, vv]))
+    assert np.array_equal(c["h_param_t"].view(torch.int16).numpy().view(np.uint16), op)
+    assert abs(sq - sq_ref) <= 1e-5 * sq_ref and bad == 0
+    with pytest.raises(Exception):
+        pipe.step([dict(desc[0], states_stride=5)], F.Hparams(step=11))
+    pipe.close()
