@@ -118,7 +118,14 @@ struct IoRequest {
 
 void CUDART_CB run_io(void* arg) {
     auto* r = static_cast<IoRequest*>(arg);
-    const std::string err = r->io->transfer(r->fd, r->buf, r->bytes, r->offset, r->write);
+    std::string err;
+    try {  // nothing may escape a CUDA host callback
+        err = r->io->transfer(r->fd, r->buf, r->bytes, r->offset, r->write);
+    } catch (const std::exception& e) {
+        err = std::string("file tier IO: ") + e.what();
+    } catch (...) {
+        err = "file tier IO: unknown exception";
+    }
     if (!err.empty()) {
         std::lock_guard<std::mutex> lk(*r->error_mu);
         r->error->store(1);
@@ -136,8 +143,13 @@ public:
         fd_ = ::open(path.c_str(), flags, 0600);
         if (fd_ < 0 && direct) fd_ = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
         if (fd_ < 0) throw InfeasibleError("cannot open tier file " + path + ": " + std::strerror(errno));
-        if (::ftruncate(fd_, static_cast<off_t>(size)) != 0)
-            throw InfeasibleError("cannot size tier file " + path + ": " + std::strerror(errno));
+        if (::ftruncate(fd_, static_cast<off_t>(size)) != 0) {
+            const std::string why = std::strerror(errno);
+            ::close(fd_);
+            ::unlink(path_.c_str());
+            fd_ = -1;
+            throw InfeasibleError("cannot size tier file " + path + ": " + why);
+        }
     }
     ~TierFile() {
         if (fd_ >= 0) ::close(fd_);
