@@ -126,6 +126,10 @@ fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad
  *         0 = 8; 6 stages only with 8). Default: path 1, 3 stages, 8 warps
  *         (measured best, profiles/). */
 fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
+/* Path 1 sweep variants for bf16 grads -> bf16 params with 8 consumer warps
+ * and 2/3/4 stages: `tile` elements per stage (1024, 2048 = default, 4096);
+ * `split` = 1 gives the loads and the stores a DMA warp each. */
+fy_status fy_adamw_tune_bulk(int tile, int split);
 
 /* Number of SMs and the launch geometry the kernels use on `device`
  * (diagnostics / roofline bookkeeping). */

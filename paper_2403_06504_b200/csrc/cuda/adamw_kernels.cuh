@@ -73,6 +73,9 @@ Geometry geometry(int device);
 // (0 = occupancy limit); path 1 = TMA bulk kernel with `unroll` pipeline
 // stages (3 or 6).
 void set_tuning(int path, int unroll, int ctas_per_sm);
+// TMA path sweep variants (bf16 -> bf16, 8 consumer warps): elements per
+// stage (1024 | 2048 | 4096) and separate load / store DMA warps.
+void set_bulk_variant(int tile, int split);
 
 // NUMA-local pinned host memory (host_mem.cu). device_numa_node: the GPU's
 // node from PCI sysfs (-1 unknown). host_alloc: page-locked, portable,

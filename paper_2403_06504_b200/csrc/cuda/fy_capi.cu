@@ -256,6 +256,13 @@ fy_status fy_host_numa_node(const void* p, int* node) {
 
 } // extern "C"
 
+extern "C" fy_status fy_adamw_tune_bulk(int tile, int split) {
+    if (tile != 1024 && tile != 2048 && tile != 4096) return fail(FY_ERR_CONFIG, "tile must be 1024, 2048 or 4096");
+    if (split != 0 && split != 1) return fail(FY_ERR_CONFIG, "split must be 0 or 1");
+    fy::set_bulk_variant(tile, split);
+    return FY_OK;
+}
+
 extern "C" fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm) {
     if (path != 0 && path != 1) return fail(FY_ERR_CONFIG, "path must be 0 (LSU) or 1 (TMA bulk)");
     if (path == 0 && unroll != 1 && unroll != 2 && unroll != 4 && unroll != 8)
