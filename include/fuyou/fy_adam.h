@@ -128,8 +128,12 @@ fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad
 fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
 /* Path 1 sweep variants for bf16 grads -> bf16 params with 8 consumer warps
  * and 2/3/4 stages: `tile` elements per stage (1024, 2048 = default, 4096);
- * `split` = 1 gives the loads and the stores a DMA warp each. */
-fy_status fy_adamw_tune_bulk(int tile, int split);
+ * `split` = 1 gives the loads and the stores a DMA warp each. `probe`
+ * (3 stages x 2048 only): 1 = L2 evict_first cache hints on the bulk
+ * copies; 2 = the same traffic with the arithmetic skipped (states written
+ * back unchanged: a speed-of-light measurement, not an optimizer step);
+ * 3 = both. 0 = off (default). */
+fy_status fy_adamw_tune_bulk(int tile, int split, int probe);
 
 /* Number of SMs and the launch geometry the kernels use on `device`
  * (diagnostics / roofline bookkeeping). */

@@ -87,7 +87,7 @@ def _load() -> C.CDLL:
         "fy_grad_stats": (st, [C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_void_p, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p]),
         "fy_adamw_tune": (st, [C.c_int, C.c_int, C.c_int]),
-        "fy_adamw_tune_bulk": (st, [C.c_int, C.c_int]),
+        "fy_adamw_tune_bulk": (st, [C.c_int, C.c_int, C.c_int]),
         "fy_device_info": (st, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]),
         "fy_shard_range": (st, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,

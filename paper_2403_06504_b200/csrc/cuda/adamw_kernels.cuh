@@ -74,8 +74,10 @@ Geometry geometry(int device);
 // stages (3 or 6).
 void set_tuning(int path, int unroll, int ctas_per_sm);
 // TMA path sweep variants (bf16 -> bf16, 8 consumer warps): elements per
-// stage (1024 | 2048 | 4096) and separate load / store DMA warps.
-void set_bulk_variant(int tile, int split);
+// stage (1024 | 2048 | 4096) and separate load / store DMA warps; probe
+// (3 stages x 2048): 1 = L2 evict_first hints, 2 = no arithmetic (the
+// access pattern's speed of light; NOT an optimizer), 3 = both.
+void set_bulk_variant(int tile, int split, int probe);
 
 // NUMA-local pinned host memory (host_mem.cu). device_numa_node: the GPU's
 // node from PCI sysfs (-1 unknown). host_alloc: page-locked, portable,

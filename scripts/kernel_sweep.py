@@ -31,11 +31,14 @@ configs = ([(0, 2, 2, 2048, 0)] + [(1, st, 0, 2048, 0) for st in (2, 3, 4)]
            + [(1, st, 4, 2048, 0) for st in (2, 3)]
            + [(1, 3, 0, 1024, 0), (1, 2, 0, 4096, 0), (1, 3, 0, 4096, 0)]
            + [(1, st, 0, 2048, 1) for st in (2, 3, 4)] + [(1, 4, 0, 1024, 1), (1, 3, 0, 4096, 1)])
+configs = [c + (0,) for c in configs]
+if len(sys.argv) > 2 and sys.argv[2] == "probes":  # hints / speed of light vs the default
+    configs = [(1, 3, 0, 2048, 0, p) for p in (0, 1, 2, 3)]
 if len(sys.argv) > 2 and sys.argv[2] == "default-only":
-    configs = [(1, 3, 0, 2048, 0)]
-for path, unroll, cps, tile, split in configs * 2:  # two passes: run-to-run noise is part of the answer
+    configs = [(1, 3, 0, 2048, 0, 0)]
+for path, unroll, cps, tile, split, probe in configs * 2:  # two passes: run-to-run noise is part of the answer
         check(LIB.fy_adamw_tune(path, unroll, cps))
-        check(LIB.fy_adamw_tune_bulk(tile, split))
+        check(LIB.fy_adamw_tune_bulk(tile, split, probe))
         def launch(k):
             st = states[k]
             F.adamw_chunk(st[:N], st[N:2 * N], st[2 * N:], grads[k], hp, param_out=grads[k],
@@ -53,12 +56,12 @@ for path, unroll, cps, tile, split in configs * 2:  # two passes: run-to-run noi
         torch.cuda.synchronize()
         ms = ev[0].elapsed_time(ev[1]) / (reps * K)
         gbs = 28 * N / (ms * 1e-3) / 1e9
-        results.append(dict(path=path, unroll=unroll, ctas_per_sm=cps, tile=tile, split=split, ms=ms,
+        results.append(dict(path=path, unroll=unroll, ctas_per_sm=cps, tile=tile, split=split, probe=probe, ms=ms,
                             gbs=gbs, frac=gbs / peak))
-        print(f"path={path} unroll={unroll} ctas_per_sm={cps} tile={tile} split={split}: {ms:.3f} ms/launch  "
+        print(f"path={path} unroll={unroll} ctas_per_sm={cps} tile={tile} split={split} probe={probe}: {ms:.3f} ms/launch  "
               f"{gbs:.0f} GB/s  {gbs / peak:.3f} of peak", flush=True)
 check(LIB.fy_adamw_tune(1, 3, 0))
-check(LIB.fy_adamw_tune_bulk(2048, 0))
+check(LIB.fy_adamw_tune_bulk(2048, 0, 0))
 best = max(results, key=lambda r: r["gbs"])
 print("BEST", json.dumps(best))
 out = ROOT / "gpurun_out" / "kernel_sweep.json"
