@@ -43,6 +43,27 @@ def test_reference_acceptance_on_b200_core():
     assert "ACCEPTANCE: 9/9 criteria passed" in r.stdout
 
 
+def test_reference_acceptance_c8_with_this_cli():
+    """Acceptance C8's subprocess half (byte-identical reruns of plan /
+    simulate+trace / sweep / capacity / validate through the CLI binary,
+    acceptance_main.cpp:471-525) — the reference skips it when no CLI is
+    built; here it runs against this repo's CLI (tools/offsim_main.cpp, C ABI
+    only)."""
+    import os
+    cli = ROOT / "build" / "offsim"
+    if not cli.exists():
+        pytest.skip("build/offsim not built")
+    exe = ROOT / "build" / "ref_acceptance_on_b200"
+    if not exe.exists():
+        pytest.skip("ref_acceptance_on_b200 not built")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "OFFSIM_CLI": str(cli)})
+    assert r.returncode == 0, r.stdout[-2000:]
+    assert "ACCEPTANCE: 9/9 criteria passed" in r.stdout
+    c8 = [ln for ln in r.stdout.splitlines() if "C8" in ln]
+    assert c8 and not any("library level only" in ln for ln in r.stdout.splitlines())
+
+
 def test_shim_calibrated_against_reference():
     r = _run(ROOT / "oracle" / "_ref" / "ref_unit_tests")
     assert r.returncode == 0 and "54 passed" in r.stdout
