@@ -82,6 +82,7 @@ def parse():
     ap.add_argument("--streamed-pieces", type=int, default=4)
     ap.add_argument("--cpu-sample-chunks", type=int, default=2)
     ap.add_argument("--no-swap-sweep", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1 / C4-block phase")
     ap.add_argument("--no-backward-overlap", action="store_true")
     ap.add_argument("--gather", choices=["auto", "nccl", "fused"], default="auto",
                     help="N>1: the kernel's fused peer-store epilogue over symmetric memory "
@@ -634,6 +635,141 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
     }
 
 
+def configs_phase(torch, F, args):
+    """The other BASELINE configs' optimizer step on this GPU,
+    beside the C2 headline:
+
+    C1 — GPT-2-small shape, 12 chunks x 7,077,888 params, device-resident:
+         eager launches vs the whole step captured once as a CUDA graph
+         (7M-param launches are ~30 us, so launch gaps matter), and streamed
+         from pinned host memory through the pipeline.
+    C4 — one GPT-3-175B block (1,811,939,328 params): resident update, the
+         per-rank slice a 2/4/8-way shard updates (fy_shard_range; the
+         per-GPU compute of the sharded step, measured on one GPU — not a
+         multi-GPU number), and the block streamed from pinned host memory
+         as 8 strided pieces (12 + 14 B/param over PCIe).
+    Rates are params/s (and GB/s at 28 B/param resident, 26 B/param
+    streamed); CUDA events, best of the repetitions."""
+    out = {}
+    dev = torch.device("cuda")
+    hp = F.optim.Hparams()
+    ws = torch.zeros(F.optim.workspace_floats(), device=dev)
+    sq = torch.zeros(1, dtype=torch.float64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def states_for(n, seed):
+        g = torch.Generator(device=dev)
+        g.manual_seed(SEED + seed)
+        st = torch.empty(3 * n, device=dev)
+        st[:n].normal_(0, 0.02, generator=g)
+        st[n:2 * n].normal_(0, 1e-3, generator=g)
+        st[2 * n:].normal_(0, 1e-3, generator=g).square_()
+        return st, (torch.randn(n, device=dev, generator=g) * 1e-3).to(torch.bfloat16)
+
+    def timed(fn, reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(reps):
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b) * 1e-3)
+        return best
+
+    def launch(st, g, n, count=None, off=0):
+        c = n if count is None else count
+        F.optim.adamw_chunk(st[off:off + c], st[n + off:n + off + c], st[2 * n + off:2 * n + off + c],
+                            g[off:off + c], hp, param_out=g[off:off + c], grad_sq_sum=sq,
+                            accumulate_sq=True, workspace=ws, nonfinite=bad)
+
+    # ---- C1: 12 x 7.08M, eager vs CUDA graph, and streamed
+    L1, N1 = 12, 12 * 768 * 768
+    c1 = [states_for(N1, 500 + k) for k in range(L1)]
+
+    def c1_step():
+        for st, g in c1:
+            launch(st, g, N1)
+    t_eager = timed(c1_step, 20)
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        c1_step()  # warm (function attributes, occupancy queries) outside capture
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph):
+        c1_step()
+    t_graph = timed(graph.replay, 20)
+    P1 = L1 * N1
+    out["c1_resident"] = {"params": P1, "eager_ms": t_eager * 1e3, "graph_ms": t_graph * 1e3,
+                          "params_per_s": P1 / t_graph, "gbs_at_28B": 28 * P1 / t_graph / 1e9,
+                          "launches_per_step": 2 * L1,
+                          "note": "one CUDA graph replay = the 24 launches of the step"}
+    # streamed: host states, grads in HBM, params to host
+    ptrs, chunks = [], []
+    for k, (st, g) in enumerate(c1):
+        hst, hpar = C.c_void_p(), C.c_void_p()
+        F.check(F.LIB.fy_host_alloc(12 * N1, C.byref(hst)))
+        F.check(F.LIB.fy_host_alloc(2 * N1, C.byref(hpar)))
+        ptrs += [hst, hpar]
+        torch.from_numpy(np.ctypeslib.as_array((C.c_float * (3 * N1)).from_address(hst.value))).copy_(st)
+        chunks.append(dict(n=N1, h_states=hst.value, grad=g.data_ptr(), h_param=hpar.value))
+    pipe = F.optim.ChunkPipeline(N1, slots=3)
+
+    def c1_streamed():
+        pipe.step(chunks, hp)
+        pipe.wait()
+    t_s = timed(c1_streamed, 10)
+    out["c1_streamed"] = {"params_per_s": P1 / t_s, "ms": t_s * 1e3, "d2h_gbs": 14 * P1 / t_s / 1e9,
+                          "h2d_gbs": 12 * P1 / t_s / 1e9}
+    pipe.close()
+    for p in ptrs:
+        F.check(F.LIB.fy_host_free(p))
+    del c1, graph
+    torch.cuda.empty_cache()
+
+    # ---- C4: one 175B block
+    N4 = 12 * 12288 * 12288
+    st, g = states_for(N4, 600)
+    t_full = timed(lambda: launch(st, g, N4), 5)
+    c4 = {"block_params": N4, "resident_ms": t_full * 1e3, "resident_params_per_s": N4 / t_full,
+          "resident_gbs_at_28B": 28 * N4 / t_full / 1e9, "shard_slice": {}}
+    for world in (2, 4, 8):
+        off, cnt = F.optim.shard_range(N4, world, 0, 8)
+        t_sl = timed(lambda: launch(st, g, N4, cnt, off), 5)
+        c4["shard_slice"][str(world)] = {"slice_params": cnt, "ms": t_sl * 1e3,
+                                         "gbs_at_28B": 28 * cnt / t_sl / 1e9}
+    # streamed from pinned host as 8 strided pieces of the block's SoA
+    hst, hpar = C.c_void_p(), C.c_void_p()
+    F.check(F.LIB.fy_host_alloc(12 * N4, C.byref(hst)))
+    F.check(F.LIB.fy_host_alloc(2 * N4, C.byref(hpar)))
+    torch.from_numpy(np.ctypeslib.as_array((C.c_float * (3 * N4)).from_address(hst.value))).copy_(st)
+    del st
+    torch.cuda.empty_cache()
+    pieces = 8
+    n = N4 // pieces
+    pipe = F.optim.ChunkPipeline(n, slots=4)
+    desc = [dict(n=n, h_states=hst.value + 4 * q * n, states_stride=N4, grad=g.data_ptr() + 2 * q * n,
+                 h_param=hpar.value + 2 * q * n) for q in range(pieces)]
+
+    def c4_streamed():
+        pipe.step(desc, hp)
+        pipe.wait()
+    t_s = timed(c4_streamed, 3)
+    c4["streamed"] = {"ms": t_s * 1e3, "params_per_s": N4 / t_s, "d2h_gbs": 14 * N4 / t_s / 1e9,
+                      "h2d_gbs": 12 * N4 / t_s / 1e9, "pieces": pieces}
+    pipe.close()
+    F.check(F.LIB.fy_host_free(hst))
+    F.check(F.LIB.fy_host_free(hpar))
+    del g
+    torch.cuda.empty_cache()
+    out["c4_block"] = c4
+    return out
+
+
 def iteration_phase(F):
     """One whole Fuyou iteration of the GPT-2-small-shaped config C1 (b=8,
     s=1024, a100 preset plan) executed by offsim_execute: every task of the
@@ -913,6 +1049,12 @@ def main():
             cpu["torch_adamw_fused_cpu"] = f"unavailable: {e}"
     if rank == 0 and world == 1 and not args.no_streamed:
         extra["streamed"] = streamed_phase(torch, F, args, pcie)
+    if rank == 0 and world == 1 and not args.no_configs:
+        try:
+            extra["configs"] = configs_phase(torch, F, args)
+        except Exception as e:  # evidence only; never masks the headline
+            extra["configs"] = f"failed: {e}"
+            torch.cuda.empty_cache()
 
     if rank == 0 and world == 1:
         try:

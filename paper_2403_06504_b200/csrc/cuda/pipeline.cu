@@ -134,10 +134,13 @@ void ChunkPipeline::issue_h2d(std::uint32_t i) {
             check_cuda(cudaMemcpyAsync(slot.states, c.h_states, 12ull * c.n, cudaMemcpyHostToDevice,
                                        h2d_),
                        "H2D states");
-        else  // master, m, v rows of a strided SoA -> contiguous slot
-            check_cuda(cudaMemcpy2DAsync(slot.states, 4 * c.n, c.h_states, 4 * stride, 4 * c.n, 3,
-                                         cudaMemcpyHostToDevice, h2d_),
-                       "H2D states (strided)");
+        else  // master, m, v rows of a strided SoA -> contiguous slot (one copy per
+              // row: 2D copies cap the pitch, and a 175B block's rows are 7 GB apart)
+            for (int r = 0; r < 3; ++r)
+                check_cuda(cudaMemcpyAsync(slot.states + 4 * c.n * r,
+                                           static_cast<const float*>(c.h_states) + stride * r, 4 * c.n,
+                                           cudaMemcpyHostToDevice, h2d_),
+                           "H2D states (strided)");
     }
     if (cfg_.grads_on_host)
         check_cuda(cudaMemcpyAsync(slot.grad, c.grad, std::uint64_t(grad_bytes_) * c.n,
@@ -187,9 +190,10 @@ void ChunkPipeline::issue_d2h(std::uint32_t i) {
                                        d2h_),
                        "D2H states");
         else
-            check_cuda(cudaMemcpy2DAsync(c.h_states, 4 * stride, slot.states, 4 * c.n, 4 * c.n, 3,
-                                         cudaMemcpyDeviceToHost, d2h_),
-                       "D2H states (strided)");
+            for (int r = 0; r < 3; ++r)
+                check_cuda(cudaMemcpyAsync(static_cast<float*>(c.h_states) + stride * r,
+                                           slot.states + 4 * c.n * r, 4 * c.n, cudaMemcpyDeviceToHost, d2h_),
+                           "D2H states (strided)");
     }
     if (cfg_.params_to_host) {
         const void* src = cfg_.keep_params_on_device ? c.d_param : slot.param;

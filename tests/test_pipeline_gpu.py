@@ -189,8 +189,8 @@ def test_numa_local_pinned_host_memory(cuda_dev):
 @pytest.mark.parametrize("states_on_device", [False, True])
 def test_pipeline_strided_pieces_equal_whole_chunk(cuda_dev, states_on_device):
     """fy_chunk.states_stride: one chunk's SoA [master | m | v] (stride n)
-    streamed as P pieces (each piece's master/m/v rows at stride n, 2D
-    copies for host states, strided kernel pointers for device states)
+    streamed as P pieces (each piece's master/m/v rows at stride n: one copy
+    per row for host states, strided kernel pointers for device states)
     equals the oracle on the whole chunk. This is how the bench's e2e path
     splits a 13B block into pipeline units without re-laying out HBM."""
     from paper_2403_06504_b200 import optim as F
