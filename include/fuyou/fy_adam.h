@@ -102,6 +102,17 @@ uint32_t fy_adamw_workspace_floats(void);
  * grad_sq_sum is requested: the second is a one-block ordered reduction). */
 fy_status fy_adamw_chunk(const fy_adamw_args* args, void* stream);
 
+/* The same step for `count` chunks at once (multi-tensor apply): one
+ * persistent TMA launch covers up to 96 chunks (their tiles concatenated),
+ * so a step over many small blocks pays one ramp-up / drain / tail instead
+ * of one per chunk (chunks of >= 33.5M elements, where that overhead is
+ * under 2%, keep their own launch). All entries must share hp, dtypes, param_out presence
+ * and the statistics outputs (grad_sq_sum, accumulate_sq, workspace,
+ * nonfinite_flag); grad_sq_sum receives the sum over all chunks. Results
+ * per element are identical to count fy_adamw_chunk calls (the grad sum of
+ * squares up to summation order). Chunks must not overlap. */
+fy_status fy_adamw_chunks(const fy_adamw_args* list, uint32_t count, void* stream);
+
 /* Same step with the all-gather fused into the epilogue:
  * besides param_out (required: the local copy), every updated 16-bit param
  * is stored to dst[r] (r < ndst <= 8), where dst[r] points at the start of

@@ -52,10 +52,16 @@ struct AdamLaunch {
 };
 
 constexpr int kThreads = 256;
+constexpr int kMaxChunksPerLaunch = 96;  // multi-chunk launch (the 175B model has 96 blocks)
 constexpr std::uint32_t kWorkspaceFloats = 148u * 32u;
 
 // Enqueue the fused step on `stream`. Returns the CUDA launch error.
 cudaError_t launch_adamw(const AdamLaunch& a, cudaStream_t stream);
+// The same step for a list of chunks in ONE persistent TMA launch per
+// kMaxChunksPerLaunch chunks (concatenated tile space; grad_sq_sum = the sum
+// over the list, taken from list[0] like dtypes, scalars and outputs). Falls
+// back to per-chunk launches when the TMA path does not apply.
+cudaError_t launch_adamw_multi(const AdamLaunch* list, int count, cudaStream_t stream);
 
 cudaError_t launch_grad_stats(const void* grad, int grad_dtype, std::uint64_t n, float grad_scale,
                               double* grad_sq_sum, int accumulate, float* workspace,

@@ -9,7 +9,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <string>
+#include <vector>
 
 namespace {
 
@@ -62,6 +64,57 @@ uint32_t fy_adamw_workspace_floats(void) { return fy::kWorkspaceFloats; }
 fy_status fy_adamw_chunk(const fy_adamw_args* a, void* stream) {
     if (!a) return fail(FY_ERR_CONFIG, "null argument");
     return guard([&] { return fy_adamw_chunk_impl(a, stream, nullptr); });
+}
+
+fy_status fy_adamw_chunks(const fy_adamw_args* list, uint32_t count, void* stream) {
+    if (!list && count > 0) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        std::vector<fy::AdamLaunch> ls;
+        ls.reserve(count);
+        for (uint32_t i = 0; i < count; ++i) {
+            const fy_adamw_args* a = &list[i];
+            const fy_adamw_args* f = &list[0];
+            const std::string at = "chunk " + std::to_string(i) + ": ";
+            if (a->n > 0 && (!a->master || !a->exp_avg || !a->exp_avg_sq || !a->grad))
+                return fail(FY_ERR_CONFIG, at + "null argument");
+            if (!valid_grad_dtype(a->grad_dtype)) return fail(FY_ERR_CONFIG, at + "bad grad_dtype");
+            if (a->param_out && !valid_param_dtype(a->param_dtype))
+                return fail(FY_ERR_CONFIG, at + "param_dtype must be bf16 or fp16");
+            if (a->param_out && a->param_out == a->grad && a->grad_dtype == FY_FP32)
+                return fail(FY_ERR_CONFIG, at + "param_out may alias grad only for 16-bit grads");
+            if (a->grad_sq_sum && !a->workspace) return fail(FY_ERR_CONFIG, at + "grad_sq_sum requires workspace");
+            if (a->hp.step == 0) return fail(FY_ERR_CONFIG, at + "step must be >= 1");
+            if (a->grad_dtype != f->grad_dtype || (a->param_out != nullptr) != (f->param_out != nullptr) ||
+                (a->param_out && a->param_dtype != f->param_dtype))
+                return fail(FY_ERR_CONFIG, at + "dtypes / param_out presence differ from chunk 0");
+            if (std::memcmp(&a->hp, &f->hp, sizeof a->hp) != 0)
+                return fail(FY_ERR_CONFIG, at + "hyper-parameters differ from chunk 0");
+            if (a->grad_sq_sum != f->grad_sq_sum || a->workspace != f->workspace ||
+                a->nonfinite_flag != f->nonfinite_flag || a->accumulate_sq != f->accumulate_sq)
+                return fail(FY_ERR_CONFIG, at + "statistics outputs differ from chunk 0");
+            if (a->n == 0) continue;
+            fy::AdamLaunch l{};
+            l.master = a->master;
+            l.m = a->exp_avg;
+            l.v = a->exp_avg_sq;
+            l.grad = a->grad;
+            l.grad_dtype = a->grad_dtype;
+            l.param = a->param_out;
+            l.param_dtype = a->param_dtype;
+            l.n = a->n;
+            l.s = fy::make_scalars(a->hp.lr, a->hp.beta1, a->hp.beta2, a->hp.eps, a->hp.weight_decay,
+                                   a->hp.step, a->hp.adamw_mode, a->hp.bias_correction, a->hp.grad_scale);
+            l.grad_sq_sum = a->grad_sq_sum;
+            l.accumulate_sq = a->accumulate_sq;
+            l.workspace = a->workspace;
+            l.nonfinite = a->nonfinite_flag;
+            ls.push_back(l);
+        }
+        fy::check_cuda(fy::launch_adamw_multi(ls.data(), static_cast<int>(ls.size()),
+                                              static_cast<cudaStream_t>(stream)),
+                       "fy_adamw_chunks");
+        return FY_OK;
+    });
 }
 
 } // extern "C"

@@ -72,6 +72,31 @@ def adamw_chunk(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.T
     check(LIB.fy_adamw_chunk(C.byref(a), C.c_void_p(stream.cuda_stream)))
 
 
+def adamw_chunks(chunks, hp: Hparams, grad_sq_sum: Optional[torch.Tensor] = None,
+                 accumulate_sq: bool = False, workspace: Optional[torch.Tensor] = None,
+                 nonfinite: Optional[torch.Tensor] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> None:
+    """fy_adamw_chunks: one multi-chunk launch. ``chunks`` = sequence of
+    (master, exp_avg, exp_avg_sq, grad, param_out_or_None)."""
+    if stream is None:
+        stream = torch.cuda.current_stream(chunks[0][0].device)
+    arr = (AdamwArgs * len(chunks))()
+    for i, (ms, m, v, g, po) in enumerate(chunks):
+        a = arr[i]
+        a.master, a.exp_avg, a.exp_avg_sq = ms.data_ptr(), m.data_ptr(), v.data_ptr()
+        a.grad = g.data_ptr()
+        a.grad_dtype = fy_dtype(g.dtype)
+        a.param_out = _ptr(po)
+        a.param_dtype = fy_dtype(po.dtype) if po is not None else FY_BF16
+        a.n = ms.numel()
+        a.hp = hp.c()
+        a.grad_sq_sum = _ptr(grad_sq_sum)
+        a.accumulate_sq = int(accumulate_sq)
+        a.workspace = _ptr(workspace)
+        a.nonfinite_flag = _ptr(nonfinite)
+    check(LIB.fy_adamw_chunks(arr, len(chunks), C.c_void_p(stream.cuda_stream)))
+
+
 def adamw_chunk_gather(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.Tensor,
                        grad: torch.Tensor, hp: Hparams, param_out: torch.Tensor, dst_ptrs,
                        grad_sq_sum: Optional[torch.Tensor] = None,
