@@ -575,7 +575,9 @@ def resident_phase(torch, F, args, world, rank, local):
         ms_multi = a.elapsed_time(b) / args.steps
         res["multi_chunk"] = {"ms_per_step": ms_multi, "params_per_s": P / (ms_multi * 1e-3),
                               "gbs_at_28B": 28 * P / (ms_multi * 1e-3) / 1e9,
-                              "launches_per_step": 2}
+                              "launches_per_step": (2 * L if N // 2048 >= 16384 else 2 * (-(-L // 96))),
+                              "note": "fy_adamw_chunks over the 40 chunks; chunks this large keep one "
+                                      "launch each inside the call (profiles/r01z_multi_chunk_ab.txt)"}
     if not args.no_e2e:
         res["e2e"] = e2e_phase(torch, F, args, states, slice_pad, cnt, world, full)
     del states, grads, full

@@ -16,7 +16,7 @@ fi
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   (timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'adamw|reduce_partials|grad_stats' -c 400 --csv \
      --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e \
-     --no-streamed --no-cpu-baseline --no-swap-sweep > $OUT/${TAG}_ncu_launch_run.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/${TAG}_ncu_launch_run.log)
+     --no-streamed --no-cpu-baseline --no-swap-sweep --no-configs > $OUT/${TAG}_ncu_launch_run.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/${TAG}_ncu_launch_run.log)
   # single-pass DRAM traffic of the fused kernel (no replay)
   (timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
      --clock-control none -k regex:adamw_ -c 6 --csv --log-file $OUT/${TAG}_traffic.csv \
