@@ -94,6 +94,10 @@ typedef struct fy_adamw_args {
     int accumulate_sq;
     float* workspace;
     int* nonfinite_flag;
+    /* Optional device-side controls (enqueue-only clipping / overflow skip;
+     * see fy_clip_coef). NULL = off. */
+    const float* grad_scale_dev; /* effective scale = fl(hp.grad_scale * *grad_scale_dev) */
+    const int* skip_if_set;      /* *skip_if_set != 0: the launch writes nothing      */
 } fy_adamw_args;
 
 uint32_t fy_adamw_workspace_floats(void);
@@ -128,6 +132,19 @@ fy_status fy_adamw_chunk_gather(const fy_adamw_args* args, void* const* dst, uin
 fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad_scale,
                         double* grad_sq_sum, int accumulate_sq, float* workspace,
                         int* nonfinite_flag, void* stream);
+
+/* Global-norm clipping and fp16-overflow skip without a host round trip
+ * (the DeepSpeed engine clips / skips before its CPU Adam step): after a
+ * stats pass over every chunk (fy_grad_stats with the loss-scale inverse,
+ * accumulating into *grad_sq_sum and *nonfinite), one 1-thread kernel
+ * writes *scale_out = 1, or max_norm / (norm + 1e-6) when max_norm > 0 and
+ * norm = sqrt(*grad_sq_sum) exceeds it (torch clip_grad_norm_), and
+ * *skip_out = 1 when any gradient was non-finite. Pass scale_out as
+ * grad_scale_dev and skip_out as skip_if_set to the fy_adamw_chunk(s)
+ * launches of the step (with hp.grad_scale = the loss-scale inverse). All
+ * pointers are device memory; stream-ordered. */
+fy_status fy_clip_coef(const double* grad_sq_sum, const int* nonfinite, float max_norm,
+                       float* scale_out, int* skip_out, void* stream);
 
 /* Tuning of the fused kernel (diagnostics / sweeps), process-wide.
  * path 0: LSU kernel, `unroll` quads (4 elements) per thread per grid-stride

@@ -41,7 +41,7 @@ class AdamwArgs(C.Structure):
         ("grad", C.c_void_p), ("grad_dtype", C.c_int), ("param_out", C.c_void_p),
         ("param_dtype", C.c_int), ("n", C.c_uint64), ("hp", AdamHparams),
         ("grad_sq_sum", C.c_void_p), ("accumulate_sq", C.c_int), ("workspace", C.c_void_p),
-        ("nonfinite_flag", C.c_void_p),
+        ("nonfinite_flag", C.c_void_p), ("grad_scale_dev", C.c_void_p), ("skip_if_set", C.c_void_p),
     ]
 
 
@@ -89,6 +89,7 @@ def _load() -> C.CDLL:
         "fy_adamw_tune": (st, [C.c_int, C.c_int, C.c_int]),
         "fy_adamw_tune_bulk": (st, [C.c_int, C.c_int, C.c_int]),
         "fy_adamw_chunks": (st, [C.POINTER(AdamwArgs), C.c_uint32, C.c_void_p]),
+        "fy_clip_coef": (st, [C.c_void_p, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
         "fy_device_info": (st, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]),
         "fy_shard_range": (st, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,

@@ -18,6 +18,10 @@ struct AdamScalars {
     float grad_scale;
     int adamw_mode;
     int has_weight_decay;
+    // Optional device-side controls, read once per thread at kernel start
+    // (enqueue-only clipping / overflow skip, no host sync):
+    const float* scale_dev; // effective grad scale = fl(grad_scale * *scale_dev)
+    const int* skip_dev;    // *skip_dev != 0: the launch writes nothing
 };
 
 AdamScalars make_scalars(float lr, float beta1, float beta2, float eps, float weight_decay,
@@ -66,6 +70,14 @@ cudaError_t launch_adamw_multi(const AdamLaunch* list, int count, cudaStream_t s
 cudaError_t launch_grad_stats(const void* grad, int grad_dtype, std::uint64_t n, float grad_scale,
                               double* grad_sq_sum, int accumulate, float* workspace,
                               int* nonfinite, cudaStream_t stream);
+
+// Global-norm clipping coefficient and overflow flag on the device, from a
+// step's accumulated grad sum of squares (of grads already multiplied by the
+// stats pass's grad_scale): norm = sqrt(*grad_sq_sum); *scale_out = 1 when
+// max_norm <= 0 or norm <= max_norm, else max_norm / (norm + 1e-6) (torch
+// clip_grad_norm_); *skip_out = (nonfinite && *nonfinite) or norm not finite.
+cudaError_t launch_clip_coef(const double* grad_sq_sum, const int* nonfinite, float max_norm,
+                             float* scale_out, int* skip_out, cudaStream_t stream);
 
 // Grid geometry used for the device (cached per device).
 struct Geometry {

@@ -66,6 +66,18 @@ fy_status fy_adamw_chunk(const fy_adamw_args* a, void* stream) {
     return guard([&] { return fy_adamw_chunk_impl(a, stream, nullptr); });
 }
 
+fy_status fy_clip_coef(const double* grad_sq_sum, const int* nonfinite, float max_norm,
+                       float* scale_out, int* skip_out, void* stream) {
+    if (!grad_sq_sum || (!scale_out && !skip_out)) return fail(FY_ERR_CONFIG, "null argument");
+    if (!(max_norm >= 0.0f)) return fail(FY_ERR_CONFIG, "max_norm must be >= 0 (0 = no clipping)");
+    return guard([&] {
+        fy::check_cuda(fy::launch_clip_coef(grad_sq_sum, nonfinite, max_norm, scale_out, skip_out,
+                                            static_cast<cudaStream_t>(stream)),
+                       "fy_clip_coef");
+        return FY_OK;
+    });
+}
+
 fy_status fy_adamw_chunks(const fy_adamw_args* list, uint32_t count, void* stream) {
     if (!list && count > 0) return fail(FY_ERR_CONFIG, "null argument");
     return guard([&] {
@@ -108,6 +120,10 @@ fy_status fy_adamw_chunks(const fy_adamw_args* list, uint32_t count, void* strea
             l.accumulate_sq = a->accumulate_sq;
             l.workspace = a->workspace;
             l.nonfinite = a->nonfinite_flag;
+            if (a->grad_scale_dev != f->grad_scale_dev || a->skip_if_set != f->skip_if_set)
+                return fail(FY_ERR_CONFIG, at + "device-side controls differ from chunk 0");
+            l.s.scale_dev = a->grad_scale_dev;
+            l.s.skip_dev = a->skip_if_set;
             ls.push_back(l);
         }
         fy::check_cuda(fy::launch_adamw_multi(ls.data(), static_cast<int>(ls.size()),
@@ -150,6 +166,8 @@ fy_status fy_adamw_chunk_impl(const fy_adamw_args* a, void* stream, const fy::Pe
     l.accumulate_sq = a->accumulate_sq;
     l.workspace = a->workspace;
     l.nonfinite = a->nonfinite_flag;
+    l.s.scale_dev = a->grad_scale_dev;
+    l.s.skip_dev = a->skip_if_set;
     if (peers) l.peers = *peers;
     fy::check_cuda(fy::launch_adamw(l, static_cast<cudaStream_t>(stream)), "fy_adamw_chunk");
     return FY_OK;

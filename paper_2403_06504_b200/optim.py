@@ -53,8 +53,12 @@ def adamw_chunk(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.T
                 grad: torch.Tensor, hp: Hparams, param_out: Optional[torch.Tensor] = None,
                 grad_sq_sum: Optional[torch.Tensor] = None, accumulate_sq: bool = False,
                 workspace: Optional[torch.Tensor] = None, nonfinite: Optional[torch.Tensor] = None,
-                stream: Optional[torch.cuda.Stream] = None, n: Optional[int] = None) -> None:
-    """Enqueue the fused step on ``stream`` (default: torch's current stream)."""
+                stream: Optional[torch.cuda.Stream] = None, n: Optional[int] = None,
+                grad_scale_dev: Optional[torch.Tensor] = None,
+                skip_if_set: Optional[torch.Tensor] = None) -> None:
+    """Enqueue the fused step on ``stream`` (default: torch's current stream).
+    grad_scale_dev (device float32[1]) / skip_if_set (device int32[1]):
+    the device-side controls written by clip_coef()."""
     if stream is None:
         stream = torch.cuda.current_stream(master.device)
     a = AdamwArgs()
@@ -69,13 +73,28 @@ def adamw_chunk(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.T
     a.accumulate_sq = int(accumulate_sq)
     a.workspace = _ptr(workspace)
     a.nonfinite_flag = _ptr(nonfinite)
+    a.grad_scale_dev = _ptr(grad_scale_dev)
+    a.skip_if_set = _ptr(skip_if_set)
     check(LIB.fy_adamw_chunk(C.byref(a), C.c_void_p(stream.cuda_stream)))
+
+
+def clip_coef(grad_sq_sum: torch.Tensor, nonfinite: Optional[torch.Tensor], max_norm: float,
+              scale_out: torch.Tensor, skip_out: torch.Tensor,
+              stream: Optional[torch.cuda.Stream] = None) -> None:
+    """fy_clip_coef: device-side clipping coefficient + overflow skip flag."""
+    if stream is None:
+        stream = torch.cuda.current_stream(grad_sq_sum.device)
+    check(LIB.fy_clip_coef(C.c_void_p(grad_sq_sum.data_ptr()), C.c_void_p(_ptr(nonfinite)),
+                           float(max_norm), C.c_void_p(scale_out.data_ptr()),
+                           C.c_void_p(skip_out.data_ptr()), C.c_void_p(stream.cuda_stream)))
 
 
 def adamw_chunks(chunks, hp: Hparams, grad_sq_sum: Optional[torch.Tensor] = None,
                  accumulate_sq: bool = False, workspace: Optional[torch.Tensor] = None,
                  nonfinite: Optional[torch.Tensor] = None,
-                 stream: Optional[torch.cuda.Stream] = None) -> None:
+                 stream: Optional[torch.cuda.Stream] = None,
+                 grad_scale_dev: Optional[torch.Tensor] = None,
+                 skip_if_set: Optional[torch.Tensor] = None) -> None:
     """fy_adamw_chunks: one multi-chunk launch. ``chunks`` = sequence of
     (master, exp_avg, exp_avg_sq, grad, param_out_or_None)."""
     if stream is None:
@@ -94,6 +113,8 @@ def adamw_chunks(chunks, hp: Hparams, grad_sq_sum: Optional[torch.Tensor] = None
         a.accumulate_sq = int(accumulate_sq)
         a.workspace = _ptr(workspace)
         a.nonfinite_flag = _ptr(nonfinite)
+        a.grad_scale_dev = _ptr(grad_scale_dev)
+        a.skip_if_set = _ptr(skip_if_set)
     check(LIB.fy_adamw_chunks(arr, len(chunks), C.c_void_p(stream.cuda_stream)))
 
 

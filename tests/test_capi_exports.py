@@ -107,6 +107,10 @@ def test_argument_validation_without_gpu():
     assert LIB.fy_host_alloc_on(16, -3, C.byref(out)) == FY_ERR_CONFIG
     assert LIB.fy_device_numa_node(0, None) == FY_ERR_CONFIG
     assert LIB.fy_host_numa_node(None, None) == FY_ERR_CONFIG
+    assert LIB.fy_clip_coef(None, None, 1.0, None, None, None) == FY_ERR_CONFIG
+    assert LIB.fy_clip_coef(0x1000, None, -1.0, 0x2000, None, None) == FY_ERR_CONFIG
+    assert b"max_norm" in LIB.fy_last_error()
+    assert LIB.fy_adamw_chunks(None, 3, None) == FY_ERR_CONFIG
 
 
 def test_graph_execute_rejects_bad_input_without_gpu():
