@@ -217,6 +217,10 @@ typedef struct fy_chunk {
                                h_states (0 = n, i.e. contiguous [master|m|v]);
                                > n lets a piece of a larger chunk's SoA
                                arrays be one pipeline unit               */
+    void* update_done;    /* optional cudaEvent_t recorded right after this
+                             chunk's update (e.g. to start its all-gather
+                             on another stream while the next chunks are
+                             still streaming)                            */
 } fy_chunk;
 
 /* Per-chunk timings of the last step, in ns relative to the step start

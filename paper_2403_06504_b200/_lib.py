@@ -58,7 +58,7 @@ class Chunk(C.Structure):
     _fields_ = [
         ("n", C.c_uint64), ("h_states", C.c_void_p), ("grad", C.c_void_p),
         ("h_param", C.c_void_p), ("d_param", C.c_void_p), ("grad_ready", C.c_void_p),
-        ("states_stride", C.c_uint64),
+        ("states_stride", C.c_uint64), ("update_done", C.c_void_p),
     ]
 
 

@@ -176,6 +176,8 @@ void ChunkPipeline::issue_update(std::uint32_t i) {
     a.nonfinite = d_nonfinite_;
     check_cuda(launch_adamw(a, opt_), "adamw launch");
     check_cuda(cudaEventRecord(ev(i, kUpdEnd), opt_), "record");
+    if (c.update_done)
+        check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(c.update_done), opt_), "record update_done");
 }
 
 void ChunkPipeline::issue_d2h(std::uint32_t i) {

@@ -218,3 +218,39 @@ def test_pipeline_strided_pieces_equal_whole_chunk(cuda_dev, states_on_device):
     with pytest.raises(Exception):
         pipe.step([dict(desc[0], states_stride=5)], F.Hparams(step=11))
     pipe.close()
+
+
+def test_pipeline_update_done_events(cuda_dev):
+    """fy_chunk.update_done is recorded right after the chunk's update: a
+    side stream that waits on it and snapshots the chunk's device params
+    (what an overlapped all-gather would send) sees the updated values."""
+    from paper_2403_06504_b200 import optim as F
+    sizes = [1 << 21, (1 << 20) + 8, 1 << 21]
+    chunks, ref = _make_chunks(sizes, 31, cuda_dev, grads_on_host=False)
+    d_params = [torch.zeros(n, dtype=torch.bfloat16, device=cuda_dev) for n in sizes]
+    snaps = [torch.zeros(n, dtype=torch.bfloat16, device=cuda_dev) for n in sizes]
+    evs = [torch.cuda.Event() for _ in sizes]
+    for e in evs:
+        e.record()  # torch creates the CUDA event lazily, on first record
+    desc = _desc(chunks)
+    for d, p, e in zip(desc, d_params, evs):
+        d["d_param"] = p.data_ptr()
+        d["update_done"] = e.cuda_event
+    pipe = F.ChunkPipeline(max(sizes), slots=2, params_to_host=True, keep_params_on_device=True)
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    pipe.step(desc, F.Hparams(step=10))
+    for p, s, e in zip(d_params, snaps, evs):
+        side.wait_event(e)
+        with torch.cuda.stream(side):
+            s.copy_(p)
+    pipe.wait()
+    torch.cuda.synchronize()
+    sc = O.scalars(step=10)
+    for s, r in zip(snaps, ref):
+        n = r["grad"].size
+        st = r["states"]
+        op = np.zeros(n, np.uint16)
+        O.adamw_step(st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy(), r["grad"], O.BF16, sc, param_out=op)
+        assert np.array_equal(s.cpu().view(torch.int16).numpy().view(np.uint16), op)
+    pipe.close()
