@@ -17,4 +17,13 @@ SEL="bit_exact and (4099 or 1048579) or tma_bulk_path_bit_exact and 14341 or ali
    python -m pytest tests/test_adamw_gpu.py -q -x -k "tma_bulk_path_bit_exact and 14341" > $OUT/${TAG}_synccheck.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_synccheck.log)
 (timeout 1200 $CS --tool memcheck --error-exitcode 9 \
    python -m pytest tests/test_executor_gpu.py -q -x -k "c1_overlapped_host_tier or swap_only" > $OUT/${TAG}_memcheck_executor.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_executor.log)
+# round-1 session-2 additions: multi-chunk list kernel, device-side clip /
+# skip controls, TMA sweep variants (split DMA warps, tiles, L2 hints)
+NEW="multi_chunk_launch_bit_exact or batches_over_96 or device_side_clipping or sweep_variants and 22541"
+(timeout 900 $CS --tool memcheck --error-exitcode 9 \
+   python -m pytest tests/test_adamw_gpu.py -q -x -k "$NEW" > $OUT/${TAG}_memcheck_new_kernels.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_new_kernels.log)
+(timeout 900 $CS --tool racecheck --error-exitcode 9 \
+   python -m pytest tests/test_adamw_gpu.py -q -x -k "multi_chunk_launch_bit_exact and tma or sweep_variants and 22541" > $OUT/${TAG}_racecheck_new_kernels.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_racecheck_new_kernels.log)
+(timeout 900 $CS --tool synccheck --error-exitcode 9 \
+   python -m pytest tests/test_adamw_gpu.py -q -x -k "multi_chunk_launch_bit_exact and tma or sweep_variants and 22541" > $OUT/${TAG}_synccheck_new_kernels.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_synccheck_new_kernels.log)
 tail -n 3 $OUT/${TAG}_*check*.log
