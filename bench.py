@@ -57,7 +57,7 @@ METRIC = "Adam params/sec & GB/s vs HBM/host-link roofline at 1/2/4/8 B200"
 UNIT = "params/s"
 BYTES_RESIDENT = 28  # 2 grad r + 12 state r + 12 state w + 2 param w
 SEED = 20240817
-E2E_PIECES = 4  # pipeline units per block in the e2e path
+E2E_PIECES = 1  # pipeline units per block in the e2e path (profiles/r01ae_e2e_shape_ab.txt)
 
 
 def shape(layers: int, hidden: int):
@@ -609,8 +609,8 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
     # all-gather assembles the rest (no extra host round trip)
     rank = dist.get_rank() if world > 1 else 0
     # each block is fed to the pipeline as E2E_PIECES units (8-aligned; the
-    # SoA states stay where they are, fy_chunk.states_stride = slice), so the
-    # copy engines fill and drain at piece granularity
+    # SoA states stay where they are, fy_chunk.states_stride = slice); whole
+    # blocks measured best (profiles/r01ae_e2e_shape_ab.txt)
     bounds = [min(n, (n * q // E2E_PIECES + 7) // 8 * 8) for q in range(E2E_PIECES)] + [n]
     spans = [(a, b) for a, b in zip(bounds, bounds[1:]) if b > a]
     pipe = F.optim.ChunkPipeline(max(b - a for a, b in spans), slots=4, grads_on_host=True,
