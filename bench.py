@@ -932,6 +932,49 @@ def iteration_phase(F):
     return out
 
 
+def swap_engine_phase(torch, F, blocks_cpu=40, blocks_ssd=8):
+    """The activation swap engine as a framework calls it (fy_swapper_*):
+    per-block checkpoints of the 13B shape at s=2048, b=8, 1-byte activations
+    (b*s*h = 83.9 MB each, the C5 b=8 plan's checkpoint size), swapped out in
+    forward order and back in reverse (backward) order, CPU placement for all
+    40 blocks and SSD placement (O_DIRECT file through the pinned ring) for a
+    bounded number of blocks; GB/s per direction on the host clock, every
+    restored buffer compared byte for byte."""
+    dev = torch.device("cuda")
+    nbytes = 8 * 2048 * 5120
+    out = {"checkpoint_bytes": nbytes}
+    for name, blocks, placement in (("cpu", blocks_cpu, F.optim.Swapper.CPU),
+                                    ("ssd", blocks_ssd, F.optim.Swapper.SSD)):
+        sw = F.optim.Swapper(slot_bytes=64 << 20, slots=4, file_dir="/tmp")
+        src = [torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev) for _ in range(blocks)]
+        back = [torch.empty_like(t) for t in src]
+        # warm the pinned buffers / file once
+        hs = [sw.swap_out(t, placement) for t in src]
+        sw.sync()
+        for h in hs:
+            sw.release(h)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hs = [sw.swap_out(t, placement) for t in src]
+        sw.sync()
+        t1 = time.perf_counter()
+        for h, t in zip(reversed(hs), reversed(back)):
+            sw.swap_in(h, t)
+        sw.sync()
+        t2 = time.perf_counter()
+        ok = all(torch.equal(a, b) for a, b in zip(src, back))
+        st = sw.stats()
+        for h in hs:
+            sw.release(h)
+        sw.close()
+        total = blocks * nbytes
+        out[name] = {"blocks": blocks, "bytes": total, "out_gbs": total / (t1 - t0) / 1e9,
+                     "in_gbs": total / (t2 - t1) / 1e9, "bit_exact": ok, "io_engine": st["io_engine"]}
+        del src, back
+    torch.cuda.empty_cache()
+    return out
+
+
 def swap_sweep_phase(F, budget_cpu=8e9, budget_ssd=2e9):
     """BASELINE config 5: activation swap GPU->host(->SSD) bandwidth sweep,
     13B shape, s=2048, b in {8,16,32,64}, swap amounts chosen by the
@@ -1188,6 +1231,10 @@ def main():
                 extra["swap_sweep"] = swap_sweep_phase(F)
             except Exception as e:
                 extra["swap_sweep"] = f"failed: {e}"
+            try:
+                extra["swap_engine"] = swap_engine_phase(torch, F)
+            except Exception as e:
+                extra["swap_engine"] = f"failed: {e}"
     if args.shard_blocks > 0 and not args.no_streamed:
         try:
             extra["streamed_shard"] = streamed_shard_phase(

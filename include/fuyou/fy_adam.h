@@ -20,7 +20,7 @@
  *                           opt update gK -> opt state_c2s gK / opt
  *                           param_c2s gK` with the depth-2 read gate
  *                           (proj/src/task_graph.cpp:453-503)
- *   fy_swap_*            <- activation swap transfers `fwd act_g2c/act_c2s`,
+ *   fy_swap_out / _in    <- activation swap transfers `fwd act_g2c/act_c2s`,
  *                           `fwd ckpt_g2c/ckpt_c2s`, `bwd ckpt_s2c/ckpt_c2g`,
  *                           `bwd act_s2c/act_c2g`
  *                           (proj/src/task_graph.cpp:296-321,357-397)
@@ -256,6 +256,46 @@ fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32
  * chunk_count 0 = synthetic states. */
 fy_status fy_graph_execute(const char* scenario_json, const char* exec_opts_json,
                            const fy_chunk* chunks, uint32_t chunk_count, char** summary_json_out);
+
+/* ------------------------------------------------------------------ */
+/* Activation swap engine: the GPU -> pinned host (-> SSD) copy path of the
+ * reference's activation swap tasks (`fwd act_g2c/act_c2s`, `fwd
+ * ckpt_g2c/ckpt_c2s`, `bwd ckpt_s2c/ckpt_c2g`, `bwd act_s2c/act_c2g`,
+ * proj/src/task_graph.cpp:296-321,357-397), callable by a training
+ * framework. placement = the planner's checkpoint location
+ * (proj/src/runner.cpp:90-106): FY_SWAP_CPU keeps the bytes in NUMA-local
+ * pinned memory, FY_SWAP_SSD streams them through a ring of `slots` pinned
+ * buffers of `slot_bytes` into an O_DIRECT file under `file_dir` (io_uring).
+ * All calls only ENQUEUE work (two copy streams + an IO stream); ordering
+ * with the caller uses CUDA events: `ready` (optional) is waited on before
+ * reading the source / writing the destination, `src_free` is recorded when
+ * the swapped-out device buffer may be reused, `done` when the swapped-in
+ * data is on the device. A swapper is used by one thread at a time. */
+typedef struct fy_swapper fy_swapper;
+enum { FY_SWAP_CPU = 0, FY_SWAP_SSD = 1 };
+typedef struct fy_swap_config {
+    int device;
+    uint64_t slot_bytes;  /* SSD ring slot size (0: 64 MiB; rounded to 4 KiB) */
+    uint32_t slots;       /* ring slots (0: 4; >= 2)                          */
+    const char* file_dir; /* NULL: /tmp                                       */
+    int direct_io;        /* O_DIRECT for the swap file                       */
+} fy_swap_config;
+
+fy_status fy_swapper_create(const fy_swap_config* cfg, fy_swapper** out);
+void fy_swapper_destroy(fy_swapper* s);
+fy_status fy_swap_out(fy_swapper* s, const void* dev_src, uint64_t bytes, int placement,
+                      void* ready_event, void* src_free_event, uint64_t* handle_out);
+fy_status fy_swap_in(fy_swapper* s, uint64_t handle, void* dev_dst, void* ready_event,
+                     void* done_event);
+/* Frees the handle's host buffer / file region (blocks until its queued
+ * copies finished). */
+fy_status fy_swap_release(fy_swapper* s, uint64_t handle);
+/* Blocks until all queued swaps finished; reports file IO errors. */
+fy_status fy_swapper_sync(fy_swapper* s);
+/* Pinned host bytes allocated for CPU placement, bytes currently laid out
+ * in the swap file, and the IO engine ("io_uring" | "pread/pwrite"). */
+fy_status fy_swapper_stats(const fy_swapper* s, uint64_t* host_bytes, uint64_t* file_bytes,
+                           const char** io_engine);
 
 /* Pinned host allocation (page-locked, portable) on the NUMA node of the
  * GPU that will stream it — the host tier's "NUMA-local pinned memory"

@@ -62,6 +62,16 @@ class Chunk(C.Structure):
     ]
 
 
+class SwapConfig(C.Structure):
+    _fields_ = [
+        ("device", C.c_int), ("slot_bytes", C.c_uint64), ("slots", C.c_uint32),
+        ("file_dir", C.c_char_p), ("direct_io", C.c_int),
+    ]
+
+
+FY_SWAP_CPU, FY_SWAP_SSD = 0, 1
+
+
 class ChunkTiming(C.Structure):
     _fields_ = [
         ("h2d_start_ns", C.c_uint64), ("h2d_end_ns", C.c_uint64),
@@ -103,6 +113,15 @@ def _load() -> C.CDLL:
                                      C.POINTER(C.c_uint64)]),
         "fy_host_alloc": (st, [C.c_uint64, C.POINTER(C.c_void_p)]),
         "fy_host_free": (st, [C.c_void_p]),
+        "fy_swapper_create": (st, [C.POINTER(SwapConfig), C.POINTER(C.c_void_p)]),
+        "fy_swapper_destroy": (None, [C.c_void_p]),
+        "fy_swap_out": (st, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p,
+                             C.POINTER(C.c_uint64)]),
+        "fy_swap_in": (st, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "fy_swap_release": (st, [C.c_void_p, C.c_uint64]),
+        "fy_swapper_sync": (st, [C.c_void_p]),
+        "fy_swapper_stats": (st, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                  C.POINTER(C.c_char_p)]),
         "fy_host_alloc_on": (st, [C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]),
         "fy_device_numa_node": (st, [C.c_int, C.POINTER(C.c_int)]),
         "fy_host_numa_node": (st, [C.c_void_p, C.POINTER(C.c_int)]),

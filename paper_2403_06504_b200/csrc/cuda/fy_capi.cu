@@ -6,6 +6,7 @@
 
 #include "adamw_kernels.cuh"
 #include "pipeline.cuh"
+#include "swap.cuh"
 
 #include <cuda_runtime.h>
 
@@ -275,6 +276,65 @@ fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32
         p->impl.timings(out, count, step_ns);
         return FY_OK;
     });
+}
+
+struct fy_swapper {
+    fy::Swapper impl;
+    explicit fy_swapper(const fy_swap_config& c) : impl(c) {}
+};
+
+fy_status fy_swapper_create(const fy_swap_config* cfg, fy_swapper** out) {
+    if (!cfg || !out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        *out = new fy_swapper(*cfg);
+        return FY_OK;
+    });
+}
+
+void fy_swapper_destroy(fy_swapper* s) { delete s; }
+
+fy_status fy_swap_out(fy_swapper* s, const void* dev_src, uint64_t bytes, int placement, void* ready_event,
+                      void* src_free_event, uint64_t* handle_out) {
+    if (!s || !dev_src || !handle_out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        *handle_out = s->impl.swap_out(dev_src, bytes, placement, static_cast<cudaEvent_t>(ready_event),
+                                       static_cast<cudaEvent_t>(src_free_event));
+        return FY_OK;
+    });
+}
+
+fy_status fy_swap_in(fy_swapper* s, uint64_t handle, void* dev_dst, void* ready_event, void* done_event) {
+    if (!s || !dev_dst) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.swap_in(handle, dev_dst, static_cast<cudaEvent_t>(ready_event),
+                        static_cast<cudaEvent_t>(done_event));
+        return FY_OK;
+    });
+}
+
+fy_status fy_swap_release(fy_swapper* s, uint64_t handle) {
+    if (!s) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.release(handle);
+        return FY_OK;
+    });
+}
+
+fy_status fy_swapper_sync(fy_swapper* s) {
+    if (!s) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.sync();
+        return FY_OK;
+    });
+}
+
+fy_status fy_swapper_stats(const fy_swapper* s, uint64_t* host_bytes, uint64_t* file_bytes,
+                           const char** io_engine) {
+    if (!s) return fail(FY_ERR_CONFIG, "null argument");
+    if (host_bytes) *host_bytes = s->impl.host_bytes();
+    if (file_bytes) *file_bytes = s->impl.file_bytes();
+    if (io_engine) *io_engine = s->impl.io_engine();
+    return FY_OK;
 }
 
 fy_status fy_host_alloc_on(uint64_t bytes, int numa_node, void** out) {

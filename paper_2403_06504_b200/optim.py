@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import torch
 
 from ._lib import (LIB, AdamHparams, AdamwArgs, Chunk, ChunkTiming, FY_BF16, FY_FP16, FY_FP32,
-                   PipelineConfig, check)
+                   FY_SWAP_CPU, FY_SWAP_SSD, PipelineConfig, SwapConfig, check)
 
 _DT = {torch.bfloat16: FY_BF16, torch.float16: FY_FP16, torch.float32: FY_FP32}
 
@@ -211,3 +211,51 @@ class ChunkPipeline:
         check(LIB.fy_pipeline_timings(self._h, arr, count, C.byref(total)))
         return [dict(h2d=(t.h2d_start_ns, t.h2d_end_ns), upd=(t.upd_start_ns, t.upd_end_ns),
                      d2h=(t.d2h_start_ns, t.d2h_end_ns)) for t in arr], total.value
+
+
+class Swapper:
+    """Activation swap engine (fy_swapper_*): GPU -> pinned host (-> SSD)."""
+    CPU, SSD = FY_SWAP_CPU, FY_SWAP_SSD
+
+    def __init__(self, device: int = 0, slot_bytes: int = 0, slots: int = 0,
+                 file_dir: str = "/tmp", direct_io: bool = True):
+        self._dir = file_dir.encode()
+        cfg = SwapConfig(device, slot_bytes, slots, self._dir, int(direct_io))
+        h = C.c_void_p()
+        check(LIB.fy_swapper_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def _ev(e):
+        return None if e is None else e.cuda_event
+
+    def swap_out(self, t: torch.Tensor, placement: int, ready=None, src_free=None) -> int:
+        h = C.c_uint64()
+        check(LIB.fy_swap_out(self._h, C.c_void_p(t.data_ptr()), t.numel() * t.element_size(),
+                              placement, self._ev(ready), self._ev(src_free), C.byref(h)))
+        return h.value
+
+    def swap_in(self, handle: int, t: torch.Tensor, ready=None, done=None) -> None:
+        check(LIB.fy_swap_in(self._h, handle, C.c_void_p(t.data_ptr()), self._ev(ready), self._ev(done)))
+
+    def release(self, handle: int) -> None:
+        check(LIB.fy_swap_release(self._h, handle))
+
+    def sync(self) -> None:
+        check(LIB.fy_swapper_sync(self._h))
+
+    def stats(self):
+        hb, fb, eng = C.c_uint64(), C.c_uint64(), C.c_char_p()
+        check(LIB.fy_swapper_stats(self._h, C.byref(hb), C.byref(fb), C.byref(eng)))
+        return dict(host_bytes=hb.value, file_bytes=fb.value, io_engine=eng.value.decode())
+
+    def close(self):
+        if self._h:
+            LIB.fy_swapper_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

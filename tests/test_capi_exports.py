@@ -111,6 +111,12 @@ def test_argument_validation_without_gpu():
     assert LIB.fy_clip_coef(0x1000, None, -1.0, 0x2000, None, None) == FY_ERR_CONFIG
     assert b"max_norm" in LIB.fy_last_error()
     assert LIB.fy_adamw_chunks(None, 3, None) == FY_ERR_CONFIG
+    assert LIB.fy_swapper_create(None, None) == FY_ERR_CONFIG
+    h = C.c_uint64()
+    assert LIB.fy_swap_out(None, None, 16, 0, None, None, C.byref(h)) == FY_ERR_CONFIG
+    assert LIB.fy_swap_in(None, 1, None, None, None) == FY_ERR_CONFIG
+    assert LIB.fy_swap_release(None, 1) == FY_ERR_CONFIG
+    assert LIB.fy_swapper_sync(None) == FY_ERR_CONFIG
 
 
 def test_graph_execute_rejects_bad_input_without_gpu():
