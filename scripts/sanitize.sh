@@ -26,4 +26,6 @@ NEW="multi_chunk_launch_bit_exact or batches_over_96 or device_side_clipping or 
    python -m pytest tests/test_adamw_gpu.py -q -x -k "multi_chunk_launch_bit_exact and tma or sweep_variants and 22541" > $OUT/${TAG}_racecheck_new_kernels.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_racecheck_new_kernels.log)
 (timeout 900 $CS --tool synccheck --error-exitcode 9 \
    python -m pytest tests/test_adamw_gpu.py -q -x -k "multi_chunk_launch_bit_exact and tma or sweep_variants and 22541" > $OUT/${TAG}_synccheck_new_kernels.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_synccheck_new_kernels.log)
+(timeout 900 $CS --tool memcheck --error-exitcode 9 \
+   python -m pytest tests/test_swap_gpu.py -q -x > $OUT/${TAG}_memcheck_swap.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_swap.log)
 tail -n 3 $OUT/${TAG}_*check*.log
