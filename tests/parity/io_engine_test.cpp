@@ -13,8 +13,38 @@
 #include <cstring>
 #include <string>
 
+// Fault injection (SURVEY.md §5 failure detection): a write through a
+// read-only descriptor and a read past the end of a short file must both
+// come back as error strings — never a crash, a hang or silent short data.
+// Prints "<engine> FAULTS-REPORTED <write error> | <read error>".
+static int faults(const std::string& dir, unsigned depth) {
+    const std::string path = dir + "/io_engine_fault.bin";
+    void* buf = nullptr;
+    const std::uint64_t bytes = 8ull << 20;
+    if (posix_memalign(&buf, 4096, bytes)) return 3;
+    std::memset(buf, 0x5A, bytes);
+    int fd = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
+    if (fd < 0) return 4;
+    if (::write(fd, buf, 1u << 20) != (1 << 20)) return 5;  // a 1 MiB file
+    ::close(fd);
+    fy::IoEngine io(depth, 1ull << 20);
+    fd = ::open(path.c_str(), O_RDONLY);
+    const std::string werr = io.transfer(fd, buf, bytes, 0, true);   // EBADF
+    const std::string rerr = io.transfer(fd, buf, bytes, 0, false);  // 7 MiB past EOF
+    ::close(fd);
+    ::unlink(path.c_str());
+    std::free(buf);
+    if (werr.empty() || rerr.empty()) {
+        std::printf("%s NOT-REPORTED [%s] [%s]\n", io.engine(), werr.c_str(), rerr.c_str());
+        return 1;
+    }
+    std::printf("%s FAULTS-REPORTED %s | %s\n", io.engine(), werr.c_str(), rerr.c_str());
+    return 0;
+}
+
 int main(int argc, char** argv) {
     if (argc < 3) return 2;
+    if (std::string(argv[2]) == "fault") return faults(argv[1], argc > 3 ? std::atoi(argv[3]) : 8);
     const std::string path = std::string(argv[1]) + "/io_engine_test.bin";
     const std::uint64_t bytes = std::strtoull(argv[2], nullptr, 10) << 20;
     const unsigned depth = argc > 3 ? static_cast<unsigned>(std::atoi(argv[3])) : 32;

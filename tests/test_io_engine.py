@@ -20,3 +20,16 @@ def test_io_engine_round_trip(tmp_path, mib, depth):
     engine, status = r.stdout.split()[:2]
     assert status == "OK"
     assert engine in ("io_uring", "pread/pwrite")
+
+
+@pytest.mark.parametrize("depth", [1, 8])
+def test_io_engine_reports_injected_faults(tmp_path, depth):
+    """A write through a read-only fd and a read past EOF are reported as
+    errors (never a crash or silent short data) — the executor turns them
+    into OFFSIM_ERR_INFEASIBLE / FY_ERR_DEVICE."""
+    if not EXE.exists():
+        pytest.skip("build/io_engine_test not built")
+    r = subprocess.run([str(EXE), str(tmp_path), "fault", str(depth)], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAULTS-REPORTED" in r.stdout

@@ -92,3 +92,20 @@ def test_swap_rejects_bad_use(cuda_dev, tmp_path):
     sw.close()
     with pytest.raises(FyError):
         F.Swapper(slots=1)
+
+
+def test_swap_reports_unusable_swap_dir(cuda_dev):
+    """Fault injection: an SSD swap into a directory that does not exist is a
+    reported error (FY_ERR_DEVICE), and CPU placement keeps working."""
+    from paper_2403_06504_b200 import optim as F
+    from paper_2403_06504_b200._lib import FyError
+    sw = F.Swapper(file_dir="/nonexistent/fy_swap_dir")
+    t = torch.arange(4096, dtype=torch.int32, device=cuda_dev).view(torch.uint8)
+    with pytest.raises(FyError):
+        sw.swap_out(t, F.Swapper.SSD)
+    h = sw.swap_out(t, F.Swapper.CPU)
+    back = torch.zeros_like(t)
+    sw.swap_in(h, back)
+    sw.sync()
+    assert torch.equal(back, t)
+    sw.close()
