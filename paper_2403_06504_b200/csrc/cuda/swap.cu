@@ -98,18 +98,32 @@ void Swapper::open_file() {
     fd_ = ::open(path_.c_str(), flags, 0600);
     if (fd_ < 0 && cfg_.direct_io) fd_ = ::open(path_.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
     if (fd_ < 0) throw DeviceError("swapper: cannot open " + path_ + ": " + std::strerror(errno));
-    // the pinned ring (SSD placement only)
-    int dev = 0;
-    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    for (std::uint32_t i = 0; i < cfg_.slots; ++i) {
-        void* p = host_alloc(cfg_.slot_bytes, device_numa_node(dev), nullptr);
-        if (!p) check_cuda(cudaHostAlloc(&p, cfg_.slot_bytes, cudaHostAllocPortable), "swap ring");
-        slots_.push_back(p);
-        cudaEvent_t a, b;
-        check_cuda(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
-        check_cuda(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
-        slot_free_.push_back(a);
-        slot_filled_.push_back(b);
+    // the pinned ring (SSD placement only); all or nothing
+    try {
+        int dev = 0;
+        check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+        for (std::uint32_t i = 0; i < cfg_.slots; ++i) {
+            void* p = host_alloc(cfg_.slot_bytes, device_numa_node(dev), nullptr);
+            if (!p) check_cuda(cudaHostAlloc(&p, cfg_.slot_bytes, cudaHostAllocPortable), "swap ring");
+            slots_.push_back(p);
+            cudaEvent_t a, b;
+            check_cuda(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+            slot_free_.push_back(a);
+            check_cuda(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+            slot_filled_.push_back(b);
+        }
+    } catch (...) {
+        for (void* p : slots_)
+            if (!host_free(p)) cudaFreeHost(p);
+        for (cudaEvent_t e : slot_free_) cudaEventDestroy(e);
+        for (cudaEvent_t e : slot_filled_) cudaEventDestroy(e);
+        slots_.clear();
+        slot_free_.clear();
+        slot_filled_.clear();
+        ::close(fd_);
+        ::unlink(path_.c_str());
+        fd_ = -1;
+        throw;
     }
 }
 
@@ -142,17 +156,20 @@ std::uint64_t Swapper::swap_out(const void* src, std::uint64_t bytes, int placem
     if (!src || bytes == 0) throw ArgError("swap_out: null source or zero bytes");
     if (placement != FY_SWAP_CPU && placement != FY_SWAP_SSD) throw ArgError("swap_out: bad placement");
     check_cuda(cudaSetDevice(cfg_.device), "cudaSetDevice");
+    if (placement == FY_SWAP_SSD) open_file();  // may throw: before anything is allocated
     Entry e;
     e.bytes = bytes;
     e.placement = placement;
-    check_cuda(cudaEventCreateWithFlags(&e.stored, cudaEventDisableTiming), "event");
+    if (placement == FY_SWAP_CPU) e.host = take_host(bytes, &e.host_cap);  // may throw (host memory)
+    if (const cudaError_t err = cudaEventCreateWithFlags(&e.stored, cudaEventDisableTiming); err != cudaSuccess) {
+        if (e.host) give_host(e.host, e.host_cap);
+        check_cuda(err, "event");
+    }
     if (ready) check_cuda(cudaStreamWaitEvent(d2h_, ready, 0), "wait ready");
     if (placement == FY_SWAP_CPU) {
-        e.host = take_host(bytes, &e.host_cap);
         check_cuda(cudaMemcpyAsync(e.host, src, bytes, cudaMemcpyDeviceToHost, d2h_), "swap out D2H");
         check_cuda(cudaEventRecord(e.stored, d2h_), "record");
     } else {
-        open_file();
         e.file_off = file_end_;
         file_end_ += round_up(bytes);
         for (std::uint64_t off = 0; off < bytes; off += cfg_.slot_bytes) {
