@@ -948,6 +948,7 @@ def swap_engine_phase(torch, F, blocks_cpu=40, blocks_ssd=8):
         sw = F.optim.Swapper(slot_bytes=64 << 20, slots=4, file_dir="/tmp")
         src = [torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev) for _ in range(blocks)]
         back = [torch.empty_like(t) for t in src]
+        torch.cuda.synchronize()  # the swapper's streams do not wait on torch's
         # warm the pinned buffers / file once
         hs = [sw.swap_out(t, placement) for t in src]
         sw.sync()

@@ -23,8 +23,11 @@ def test_swap_round_trip_many_handles(cuda_dev, tmp_path, placement):
     pl = F.Swapper.CPU if placement == "cpu" else F.Swapper.SSD
     sizes = [4096, 12345, (1 << 20) + 17, 5 * (1 << 20) + 4093, 3 << 20]
     src = [_pattern(n, 100 + i, cuda_dev) for i, n in enumerate(sizes)]
-    handles = [sw.swap_out(t, pl) for t in src]
     dst = [torch.zeros_like(t) for t in src]
+    # the swapper's streams do not follow torch's: without `ready` events the
+    # caller makes its producers (and the zero-fill of dst) complete first
+    torch.cuda.synchronize()
+    handles = [sw.swap_out(t, pl) for t in src]
     for h, t in zip(reversed(handles), reversed(dst)):  # backward order, like the schedule
         sw.swap_in(h, t)
     sw.sync()
@@ -66,7 +69,9 @@ def test_swap_event_ordering(cuda_dev, tmp_path, placement):
         prod.wait_event(src_free)
         act.fill_(0)  # the device buffer is reused for something else
     back = torch.zeros(n, dtype=torch.uint8, device=cuda_dev)
-    sw.swap_in(h, back, done=done)
+    back_ready = torch.cuda.Event()
+    back_ready.record()  # the zero-fill of `back` is queued on torch's stream
+    sw.swap_in(h, back, ready=back_ready, done=done)
     cons = torch.cuda.Stream()
     cons.wait_event(done)
     with torch.cuda.stream(cons):
@@ -101,10 +106,12 @@ def test_swap_reports_unusable_swap_dir(cuda_dev):
     from paper_2403_06504_b200._lib import FyError
     sw = F.Swapper(file_dir="/nonexistent/fy_swap_dir")
     t = torch.arange(4096, dtype=torch.int32, device=cuda_dev).view(torch.uint8)
+    torch.cuda.synchronize()
     with pytest.raises(FyError):
         sw.swap_out(t, F.Swapper.SSD)
     h = sw.swap_out(t, F.Swapper.CPU)
     back = torch.zeros_like(t)
+    torch.cuda.synchronize()
     sw.swap_in(h, back)
     sw.sync()
     assert torch.equal(back, t)
