@@ -229,14 +229,35 @@ class Swapper:
     def _ev(e):
         return None if e is None else e.cuda_event
 
+    @staticmethod
+    def _now(dev):
+        e = torch.cuda.Event()
+        e.record(torch.cuda.current_stream(dev))
+        return e
+
     def swap_out(self, t: torch.Tensor, placement: int, ready=None, src_free=None) -> int:
+        """Default `ready`: everything already queued on torch's current
+        stream (so a tensor just produced there is complete)."""
+        if ready is None:
+            ready = self._now(t.device)
         h = C.c_uint64()
         check(LIB.fy_swap_out(self._h, C.c_void_p(t.data_ptr()), t.numel() * t.element_size(),
                               placement, self._ev(ready), self._ev(src_free), C.byref(h)))
         return h.value
 
     def swap_in(self, handle: int, t: torch.Tensor, ready=None, done=None) -> None:
+        """Default `ready`: torch's current stream so far; default `done`:
+        torch's current stream waits for the restored data (stream-ordered
+        like a copy_ on it). Pass events to overlap instead."""
+        if ready is None:
+            ready = self._now(t.device)
+        wait_here = done is None
+        if wait_here:
+            done = torch.cuda.Event()
+            done.record(torch.cuda.current_stream(t.device))  # create it
         check(LIB.fy_swap_in(self._h, handle, C.c_void_p(t.data_ptr()), self._ev(ready), self._ev(done)))
+        if wait_here:
+            torch.cuda.current_stream(t.device).wait_event(done)
 
     def release(self, handle: int) -> None:
         check(LIB.fy_swap_release(self._h, handle))
