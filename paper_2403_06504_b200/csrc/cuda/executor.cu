@@ -116,7 +116,15 @@ struct IoRequest {
     std::mutex* error_mu = nullptr;
 };
 
+// Released at the end of every IO host function, acquired after the device
+// synchronisations that wait for them (the CUDA-guaranteed ordering made
+// explicit for the C++ memory model and ThreadSanitizer).
+std::atomic<std::uint64_t> g_io_done{0};
+
 void CUDART_CB run_io(void* arg) {
+    struct Done {
+        ~Done() { g_io_done.fetch_add(1, std::memory_order_release); }
+    } done;
     auto* r = static_cast<IoRequest*>(arg);
     std::string err;
     try {  // nothing may escape a CUDA host callback
@@ -238,6 +246,7 @@ public:
         cudaSetDevice(opt_.device);
         for (cudaStream_t s : streams_)
             if (s) cudaStreamSynchronize(s);
+        (void)g_io_done.load(std::memory_order_acquire);
         if (blas_) cublasDestroy(blas_);
         for (cudaEvent_t e : events_) cudaEventDestroy(e);
         if (base_) cudaEventDestroy(base_);
@@ -935,6 +944,7 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
     for (int r = 1; r < 5; ++r) check_cuda(cudaStreamWaitEvent(streams_[r], base_, 0), "base wait");
     for (const auto& [start, id] : order) issue(g_.tasks[id], rep);
     check_cuda(cudaDeviceSynchronize(), "executor run");
+    (void)g_io_done.load(std::memory_order_acquire);  // pairs with run_io's release
     if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
 
     // swap integrity: every restored buffer equals its original

@@ -23,7 +23,10 @@ std::uint64_t round_up(std::uint64_t x) { return (x + kAlign - 1) / kAlign * kAl
 void CUDART_CB run_swap_io(void* arg) {
     auto* r = static_cast<Swapper::IoReq*>(arg);
     Swapper& s = *r->self;
-    if (s.io_failed.load()) return;
+    if (s.io_failed.load()) {
+        s.io_done.fetch_add(1, std::memory_order_release);
+        return;
+    }
     std::string err;
     try {
         err = s.engine().transfer(s.fd(), r->buf, r->bytes, r->offset, r->write);
@@ -35,6 +38,7 @@ void CUDART_CB run_swap_io(void* arg) {
         s.io_error = err;
         s.io_failed.store(1);
     }
+    s.io_done.fetch_add(1, std::memory_order_release);
 }
 
 } // namespace
@@ -63,6 +67,7 @@ void Swapper::release_all() noexcept {
     if (d2h_) cudaStreamSynchronize(d2h_);
     if (h2d_) cudaStreamSynchronize(h2d_);
     if (io_s_) cudaStreamSynchronize(io_s_);
+    (void)io_done.load(std::memory_order_acquire);  // the IO host functions are done
     for (auto& [h, e] : entries_) {
         if (e.stored) cudaEventDestroy(e.stored);
         if (e.host && !host_free(e.host)) cudaFreeHost(e.host);
@@ -232,6 +237,7 @@ void Swapper::release(std::uint64_t handle) {
     // only through a new handle)
     check_cuda(cudaEventSynchronize(e.stored), "release");
     check_cuda(cudaStreamSynchronize(h2d_), "release");
+    (void)io_done.load(std::memory_order_acquire);
     cudaEventDestroy(e.stored);
     if (e.host) give_host(e.host, e.host_cap);
     bool any_file = false;
@@ -244,6 +250,7 @@ void Swapper::sync() {
     check_cuda(cudaStreamSynchronize(d2h_), "swap sync");
     check_cuda(cudaStreamSynchronize(io_s_), "swap sync");
     check_cuda(cudaStreamSynchronize(h2d_), "swap sync");
+    (void)io_done.load(std::memory_order_acquire);  // pairs with run_swap_io's release
     reqs_.clear();
     if (io_failed.load()) {
         std::lock_guard<std::mutex> lk(io_mu);

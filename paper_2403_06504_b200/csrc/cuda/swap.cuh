@@ -91,6 +91,11 @@ private:
 
 public:
     std::atomic<int> io_failed{0};
+    // Released by every IO host function when it finishes and acquired after
+    // the stream synchronisations that wait for them: makes the ordering the
+    // CUDA runtime guarantees explicit in the C++ memory model (and visible
+    // to ThreadSanitizer, which cannot see inside libcuda).
+    std::atomic<std::uint64_t> io_done{0};
     std::mutex io_mu;
     std::string io_error;
     IoEngine& engine() { return io_; }
