@@ -912,7 +912,9 @@ def iteration_phase(F):
         summ = P()
         opts = {"tier": "host", "compute_rate": 1.4e15}
         if tag.startswith("13b"):
-            opts = {"tier": "host", "compute_mode": "gemm"}  # real bf16 GEMMs beside the optimizer
+            # real bf16 GEMMs beside the optimizer; each wgrad writes its
+            # block's gradients, which the fused optimizer then consumes
+            opts = {"tier": "host", "compute_mode": "gemm_dataflow"}
         st = L.offsim_execute(h, json.dumps(opts).encode(), C.byref(summ), None)
         L.offsim_scenario_free(h)
         d = json.loads(C.cast(summ, C.c_char_p).value.decode())
@@ -928,6 +930,9 @@ def iteration_phase(F):
                     "swap_mismatches": d["swap_mismatches"],
                     "optimizer_kernel_params_per_s": d["optimizer"]["kernel_params_per_s"],
                     "launches": d["kernel_launches"], "compute_mode": opts.get("compute_mode", "spin"),
+                    "grad_dataflow_rel_err": (abs(d["optimizer"]["grad_sq_sum"] - d["optimizer"]["expected_grad_sq_sum"])
+                                              / d["optimizer"]["expected_grad_sq_sum"]
+                                              if d["optimizer"].get("expected_grad_sq_sum", -1) > 0 else None),
                     "busy_s": d["executed"]["busy_s"]}
     return out
 

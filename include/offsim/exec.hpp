@@ -67,7 +67,11 @@ struct ExecOptions {
     // fwd/bwd compute tasks: "spin" = timed kernel of work / compute_rate
     // (no SM/HBM contention); "gemm" = the layer's real bf16 GEMMs through
     // cuBLAS (fwd: one b*s x out x in GEMM; bwd: dgrad + wgrad), so the
-    // optimizer overlaps real tensor-core work (rate measured, not assumed).
+    // optimizer overlaps real tensor-core work (rate measured, not assumed);
+    // "gemm_dataflow" = "gemm" with each layer's wgrad (X^T dY) written into
+    // its block's gradient buffer, so the fused optimizer consumes the
+    // gradients the backward produced (checked against an independent
+    // computation of their norm).
     std::string compute_mode = "spin";
     std::uint32_t state_slots = 3;  // device staging slots for optimizer groups
     AdamHyper adam;
@@ -180,6 +184,10 @@ struct ExecReport {
     std::map<std::string, double> reference_bytes; // "<lane>/<payload>" of the input graph
     std::map<std::string, double> physical_bytes;  // "h2d|d2h|file_read|file_write/<payload>"
     double grad_sq_sum = 0.0;
+    // compute_mode "gemm_dataflow": the grad sum of squares the backward's
+    // wgrad GEMMs must hand the optimizer (computed independently before the
+    // run); -1 otherwise
+    double expected_grad_sq_sum = -1.0;
     int nonfinite = 0;
     std::uint64_t swap_checks = 0;     // restored buffers verified
     std::uint64_t swap_mismatches = 0; // must be 0

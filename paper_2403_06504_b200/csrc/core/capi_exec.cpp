@@ -140,6 +140,7 @@ json optimizer_json(const ExecReport& r) {
                 {"kernel_params_per_s", upd_ns > 0 ? params / (upd_ns * 1e-9) : 0.0},
                 {"window_s", last > first ? static_cast<double>(last - first) * 1e-9 : 0.0},
                 {"grad_sq_sum", r.grad_sq_sum},
+                {"expected_grad_sq_sum", r.expected_grad_sq_sum},
                 {"nonfinite", r.nonfinite}};
 }
 

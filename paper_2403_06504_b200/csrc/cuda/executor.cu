@@ -337,9 +337,14 @@ private:
     double compute_rate_ = 0.0;
     // gemm compute mode
     bool gemm_ = false;
+    bool dataflow_ = false;  // compute_mode "gemm_dataflow": wgrad GEMMs produce the optimizer's grads
     cublasHandle_t blas_ = nullptr;
     Device gemm_a_, gemm_b_, gemm_c_, gemm_ws_;
     void gemm(cudaStream_t s, int m, int n, int k);
+    // dW[in x out] = X^T dY with X = the first tokens x in of gemm_a_, dY =
+    // the first tokens x out of gemm_b_ (row-major bf16), written to dst
+    void wgrad(cudaStream_t s, int tokens, int in, int out, void* dst);
+    double expected_grad_sq_ = 0.0;  // gemm_dataflow self-check
     void layer_dims(int j, int& in, int& out) const {
         const int h = static_cast<int>(model_.hidden_dim);
         static const int kIn[4] = {1, 1, 1, 4}, kOut[4] = {3, 1, 4, 1};
@@ -479,9 +484,13 @@ void Engine::setup() {
         assign_ring_slots();
     }
 
-    gemm_ = opt_.compute_mode == "gemm";
+    dataflow_ = opt_.compute_mode == "gemm_dataflow";
+    gemm_ = opt_.compute_mode == "gemm" || dataflow_;
     if (!gemm_ && opt_.compute_mode != "spin")
-        throw ConfigError("executor: compute_mode must be 'spin' or 'gemm'");
+        throw ConfigError("executor: compute_mode must be 'spin', 'gemm' or 'gemm_dataflow'");
+    if (dataflow_ && (user_ || !has_update_ || g_.header.variant != ScheduleVariant::overlapped))
+        throw ConfigError("executor: gemm_dataflow needs synthetic states, an optimizer and the "
+                          "overlapped variant (grads stay in HBM)");
     if (gemm_) {
         const std::uint64_t tokens = model_.batch_size * model_.seq_len;
         const std::uint64_t h = model_.hidden_dim;
@@ -510,6 +519,29 @@ void Engine::setup() {
     d_mismatch_ = Device(sizeof(unsigned long long));
     check_cuda(cudaMemset(d_norm_.p, 0, sizeof(double)), "memset");
     check_cuda(cudaMemset(d_bad_.p, 0, sizeof(int)), "memset");
+    if (dataflow_) {
+        // self-check of the grad dataflow: every block's layer j gets the same
+        // dW_j = X^T dY (same operands), so the optimizer's accumulated grad
+        // sum of squares must equal blocks x sum_j |dW_j * grad_scale|^2
+        std::uint64_t max_w = 0;
+        for (int j = 0; j < 4; ++j) max_w = std::max<std::uint64_t>(max_w, layers_[j].param_bytes);
+        Device scratch(max_w), d_exp(sizeof(double));
+        const int tokens = static_cast<int>(model_.batch_size * model_.seq_len);
+        cudaStream_t s0 = lane_stream(ResourceId::gpu_compute);
+        for (int j = 0; j < 4; ++j) {
+            int in = 0, out = 0;
+            layer_dims(j, in, out);
+            wgrad(s0, tokens, in, out, scratch.p);
+            check_cuda(fy::launch_grad_stats(scratch.p, 0, std::uint64_t(in) * out, opt_.adam.grad_scale,
+                                             static_cast<double*>(d_exp.p), j > 0,
+                                             static_cast<float*>(workspace_.p), nullptr, s0),
+                       "expected grad norm");
+        }
+        double per_block = 0.0;
+        check_cuda(cudaStreamSynchronize(s0), "expected grad norm");
+        check_cuda(cudaMemcpy(&per_block, d_exp.p, sizeof(double), cudaMemcpyDeviceToHost), "expected grad norm");
+        expected_grad_sq_ = per_block * blocks_;
+    }
     check_cuda(cudaMemset(d_mismatch_.p, 0, sizeof(unsigned long long)), "memset");
 
     if (file_tier_) {
@@ -809,6 +841,17 @@ void Engine::gemm(cudaStream_t s, int m, int n, int k) {
     if (st != CUBLAS_STATUS_SUCCESS) throw fy::DeviceError("cublasGemmEx failed: status " + std::to_string(st));
 }
 
+void Engine::wgrad(cudaStream_t s, int tokens, int in, int out, void* dst) {
+    // row-major dW[in x out] = X[t x in]^T * dY[t x out]; in cuBLAS's
+    // column-major view: dW_cm[out x in] = dY_cm[out x t] * (X_cm[in x t])^T
+    cublasSetStream(blas_, s);
+    const float alpha = 1.0f, beta = 0.0f;
+    const cublasStatus_t st = cublasGemmEx(blas_, CUBLAS_OP_N, CUBLAS_OP_T, out, in, tokens, &alpha, gemm_b_.p,
+                                           CUDA_R_16BF, out, gemm_a_.p, CUDA_R_16BF, in, &beta, dst,
+                                           CUDA_R_16BF, out, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS) throw fy::DeviceError("cublasGemmEx (wgrad) failed: status " + std::to_string(st));
+}
+
 void Engine::issue(const Task& t, ExecReport& rep) {
     cudaStream_t s = lane_stream(t.resource);
     for (const std::uint32_t d : t.deps)
@@ -848,7 +891,10 @@ void Engine::issue(const Task& t, ExecReport& rep) {
         const int tokens = static_cast<int>(model_.batch_size * model_.seq_len);
         if (p.phase == "bwd" && w == "compute") {
             gemm(s, tokens, in, out);  // dgrad: dY[t x out] * W^T -> dX[t x in]
-            gemm(s, in, out, tokens);  // wgrad: X^T[in x t] * dY -> dW[in x out]
+            if (dataflow_)             // wgrad straight into the block's grad buffer (the optimizer's input)
+                wgrad(s, tokens, in, out, static_cast<char*>(const_cast<void*>(d_grads_[k])) + layer_offset(j));
+            else
+                gemm(s, in, out, tokens);  // wgrad: X^T[in x t] * dY -> dW[in x out]
         } else {
             gemm(s, tokens, out, in);  // forward / recompute
         }
@@ -967,6 +1013,7 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
         rep.swap_mismatches = bad;
     }
     check_cuda(cudaMemcpy(&rep.grad_sq_sum, d_norm_.p, sizeof(double), cudaMemcpyDeviceToHost), "norm");
+    rep.expected_grad_sq_sum = dataflow_ ? expected_grad_sq_ : -1.0;
     rep.pinned_host_bytes = pinned_bytes_;
     if (opt_.checksum_states && has_update_) rep.state_checksum = checksum_states();
     check_cuda(cudaMemcpy(&rep.nonfinite, d_bad_.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
