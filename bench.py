@@ -173,9 +173,15 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook (scripts/same_gpu_ranks.sh): several ranks on ONE GPU over a
+    # gloo group, to exercise the N>1 plumbing (symmetric-memory rendezvous,
+    # fused peer-store gather, max-over-ranks) where only one GPU exists.
+    same_gpu = os.environ.get("FY_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
+    backend = "gloo" if (same_gpu or args.impl != "b200") else "nccl"
     if (world > 1 or getattr(args, "gather", "nccl") == "fused") and not dist.is_initialized():
-        dist.init_process_group("nccl" if args.impl == "b200" else "gloo",
-                                device_id=torch.device("cuda", local) if args.impl == "b200" else None)
+        dist.init_process_group(backend, device_id=torch.device("cuda", local) if backend == "nccl" else None)
     return world, rank, local
 
 
@@ -184,7 +190,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -444,6 +451,28 @@ def streamed_backward_overlap(torch, pipe, chunks, hp, K, P, t_stream):
                         "72*t*h^2 FLOPs/block, separate stream"}
 
 
+def ipc_peer_buffers(F, nbytes, world, rank):
+    """Every rank allocates its full-param buffer with fy_ipc_alloc and
+    publishes the CUDA IPC handle; each rank opens the others' handles.
+    Returns {"ptrs": [device pointer of rank q's buffer as seen here]}."""
+    import torch.distributed as dist
+    own = C.c_void_p()
+    handle = (C.c_char * 64)()
+    F.check(F.LIB.fy_ipc_alloc(nbytes, C.byref(own), handle))
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(handle))
+    ptrs = []
+    for q in range(world):
+        if q == rank:
+            ptrs.append(own.value)
+            continue
+        p = C.c_void_p()
+        hq = (C.c_char * 64).from_buffer_copy(handles[q])
+        F.check(F.LIB.fy_ipc_open(hq, C.byref(p)))
+        ptrs.append(p.value)
+    return {"ptrs": ptrs, "own": own}
+
+
 def resident_phase(torch, F, args, world, rank, local):
     """The headline: device-resident step (value + roofline) and its e2e."""
     import torch.distributed as dist
@@ -478,11 +507,25 @@ def resident_phase(torch, F, args, world, rank, local):
             full = [big[k * world * slice_pad:(k + 1) * world * slice_pad] for k in range(L)]
             dst_ptrs = [[symm.buffer_ptrs[q] + 2 * (k * world + rank) * slice_pad
                          for q in range(world)] for k in range(L)]
-        except Exception as e:  # auto: the NCCL all-gather instead (both are device paths)
-            if args.gather == "fused":
-                raise
-            fused, symm, gather_note = False, None, f"symmetric memory unavailable ({e}); NCCL"
+        except Exception as e:
             torch.cuda.empty_cache()
+            symm = None
+            if world > 1:
+                # the same peer-store epilogue on CUDA IPC buffers (fy_ipc_*),
+                # with a host barrier per step instead of the device one
+                try:
+                    ipc = ipc_peer_buffers(F, L * world * slice_pad * 2, world, rank)
+                    dst_ptrs = [[ipc["ptrs"][q] + 2 * (k * world + rank) * slice_pad for q in range(world)]
+                                for k in range(L)]
+                    gather_note = f"symmetric memory unavailable ({str(e)[:120]}); fused epilogue over CUDA IPC"
+                except Exception as e2:  # the NCCL all-gather instead (a device path too)
+                    if args.gather == "fused":
+                        raise
+                    fused, gather_note = False, f"no peer buffers ({str(e)[:80]}; {str(e2)[:80]}); NCCL"
+            elif args.gather == "fused":
+                raise
+            else:
+                fused = False
     if world > 1 and not fused:
         full = [torch.empty(world * slice_pad, dtype=torch.bfloat16, device=dev) for _ in range(L)]
     ws = torch.zeros(F.optim.workspace_floats(), device=dev)
@@ -517,9 +560,12 @@ def resident_phase(torch, F, args, world, rank, local):
                     dist.all_gather_into_tensor(full[k], grads[k])
         if world > 1 and not fused:
             stream.wait_stream(comm)
-        if fused:
+        if fused and symm is not None:
             with torch.cuda.stream(stream):
                 symm.barrier(channel=0)  # peers' stores landed before the params are used
+        elif fused and world > 1:
+            torch.cuda.synchronize()     # IPC buffers: host barrier per step
+            dist.barrier()
 
     for w in range(args.warmup):
         one_step(w)
@@ -556,7 +602,8 @@ def resident_phase(torch, F, args, world, rank, local):
         "launches": args.steps * L * 2,  # fused Adam kernel + 1-block ordered norm reduction
         "grad_sq_sum": float(sq.item()),
         "nonfinite": int(bad.item()),
-        "gather": ("fused" if fused else "nccl") if world > 1 or fused else None,
+        "gather": (("fused-ipc" if symm is None and world > 1 else "fused") if fused else "nccl")
+                  if world > 1 or fused else None,
         "gather_note": gather_note,
     }
 
@@ -595,6 +642,8 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
     import torch.distributed as dist
     L = len(states)
     n = slice_pad
+    if world > 1 and full is None:  # IPC-gather runs keep no torch-side full buffers
+        full = [torch.empty(world * n, dtype=torch.bfloat16, device="cuda") for _ in range(L)]
     hbuf = []
     for k in range(L):
         p = C.c_void_p()

@@ -297,6 +297,18 @@ fy_status fy_swapper_sync(fy_swapper* s);
 fy_status fy_swapper_stats(const fy_swapper* s, uint64_t* host_bytes, uint64_t* file_bytes,
                            const char** io_engine);
 
+/* Peer buffers for the fused all-gather epilogue without torch symmetric
+ * memory: fy_ipc_alloc allocates device memory and writes its 64-byte CUDA
+ * IPC handle; another process opens it with fy_ipc_open (peer access enabled
+ * lazily) and passes the returned pointer (+ its slice offset) as a
+ * fy_adamw_chunk_gather destination. Close with fy_ipc_close in the opener,
+ * free with fy_ipc_free in the allocator. */
+#define FY_IPC_HANDLE_BYTES 64
+fy_status fy_ipc_alloc(uint64_t bytes, void** ptr, void* handle_out);
+fy_status fy_ipc_open(const void* handle, void** ptr);
+fy_status fy_ipc_close(void* ptr);
+fy_status fy_ipc_free(void* ptr);
+
 /* Pinned host allocation (page-locked, portable) on the NUMA node of the
  * GPU that will stream it — the host tier's "NUMA-local pinned memory"
  * (SURVEY.md §8e). fy_host_alloc: the current device's node (PCI sysfs).

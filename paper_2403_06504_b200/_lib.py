@@ -113,6 +113,10 @@ def _load() -> C.CDLL:
                                      C.POINTER(C.c_uint64)]),
         "fy_host_alloc": (st, [C.c_uint64, C.POINTER(C.c_void_p)]),
         "fy_host_free": (st, [C.c_void_p]),
+        "fy_ipc_alloc": (st, [C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]),
+        "fy_ipc_open": (st, [C.c_void_p, C.POINTER(C.c_void_p)]),
+        "fy_ipc_close": (st, [C.c_void_p]),
+        "fy_ipc_free": (st, [C.c_void_p]),
         "fy_swapper_create": (st, [C.POINTER(SwapConfig), C.POINTER(C.c_void_p)]),
         "fy_swapper_destroy": (None, [C.c_void_p]),
         "fy_swap_out": (st, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p,

@@ -337,6 +337,51 @@ fy_status fy_swapper_stats(const fy_swapper* s, uint64_t* host_bytes, uint64_t* 
     return FY_OK;
 }
 
+fy_status fy_ipc_alloc(uint64_t bytes, void** ptr, void* handle_out) {
+    if (!ptr || !handle_out || bytes == 0) return fail(FY_ERR_CONFIG, "null argument or zero bytes");
+    return guard([&] {
+        void* p = nullptr;
+        const cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaErrorMemoryAllocation)
+            return fail(FY_ERR_INFEASIBLE, "device allocation of " + std::to_string(bytes) + " bytes failed");
+        fy::check_cuda(e, "cudaMalloc (ipc)");
+        cudaIpcMemHandle_t h;
+        const cudaError_t he = cudaIpcGetMemHandle(&h, p);
+        if (he != cudaSuccess) {
+            cudaFree(p);
+            fy::check_cuda(he, "cudaIpcGetMemHandle");
+        }
+        std::memcpy(handle_out, &h, sizeof h);
+        *ptr = p;
+        return FY_OK;
+    });
+}
+
+fy_status fy_ipc_open(const void* handle, void** ptr) {
+    if (!handle || !ptr) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        fy::check_cuda(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        return FY_OK;
+    });
+}
+
+fy_status fy_ipc_close(void* ptr) {
+    if (!ptr) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        fy::check_cuda(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+        return FY_OK;
+    });
+}
+
+fy_status fy_ipc_free(void* ptr) {
+    return guard([&] {
+        if (ptr) fy::check_cuda(cudaFree(ptr), "cudaFree (ipc)");
+        return FY_OK;
+    });
+}
+
 fy_status fy_host_alloc_on(uint64_t bytes, int numa_node, void** out) {
     if (!out) return fail(FY_ERR_CONFIG, "null argument");
     if (numa_node < -2) return fail(FY_ERR_CONFIG, "numa_node must be >= -2");
