@@ -117,6 +117,9 @@ def test_argument_validation_without_gpu():
     assert LIB.fy_swap_in(None, 1, None, None, None) == FY_ERR_CONFIG
     assert LIB.fy_swap_release(None, 1) == FY_ERR_CONFIG
     assert LIB.fy_swapper_sync(None) == FY_ERR_CONFIG
+    assert LIB.fy_ipc_alloc(0, None, None) == FY_ERR_CONFIG
+    assert LIB.fy_ipc_open(None, None) == FY_ERR_CONFIG
+    assert LIB.fy_ipc_close(None) == FY_ERR_CONFIG
 
 
 def test_graph_execute_rejects_bad_input_without_gpu():
