@@ -9,3 +9,9 @@ FY_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --npr
   --warmup 3 --no-e2e --shard-blocks 0 > $OUT/same_gpu_ranks.json 2> $OUT/same_gpu_ranks.err
 echo "rc=$?" >> $OUT/same_gpu_ranks.err
 tail -5 $OUT/same_gpu_ranks.err; cat $OUT/same_gpu_ranks.json | tail -1 | cut -c1-600
+# the streamed-shard phase and the e2e path at N=2 (gloo stages the CUDA
+# all-gathers through host memory: plumbing only)
+FY_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --layers 4 --steps 3 --warmup 3 \
+  --shard-blocks 1 > $OUT/same_gpu_ranks_full.json 2> $OUT/same_gpu_ranks_full.err
+echo "rc=$?" >> $OUT/same_gpu_ranks_full.err
