@@ -162,6 +162,10 @@ fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
  * back unchanged: a speed-of-light measurement, not an optimizer step);
  * 3 = both. 0 = off (default). */
 fy_status fy_adamw_tune_bulk(int tile, int split, int probe);
+/* SM budget of the fused step (TMA path), process-wide: launches use at most
+ * max_ctas CTAs — one per SM — leaving the other SMs to a backward running
+ * concurrently on another stream (0 = every SM, the default). */
+fy_status fy_adamw_sm_budget(int max_ctas);
 
 /* Number of SMs and the launch geometry the kernels use on `device`
  * (diagnostics / roofline bookkeeping). */

@@ -96,6 +96,9 @@ void set_tuning(int path, int unroll, int ctas_per_sm);
 // (3 stages x 2048): 1 = L2 evict_first hints, 2 = no arithmetic (the
 // access pattern's speed of light; NOT an optimizer), 3 = both.
 void set_bulk_variant(int tile, int split, int probe);
+// SM budget of the TMA path: at most max_ctas CTAs (one per SM; 0 = all SMs)
+// so a concurrent backward keeps the remaining SMs.
+void set_max_ctas(int max_ctas);
 
 // NUMA-local pinned host memory (host_mem.cu). device_numa_node: the GPU's
 // node from PCI sysfs (-1 unknown). host_alloc: page-locked, portable,

@@ -432,6 +432,12 @@ fy_status fy_host_numa_node(const void* p, int* node) {
 
 } // extern "C"
 
+extern "C" fy_status fy_adamw_sm_budget(int max_ctas) {
+    if (max_ctas < 0) return fail(FY_ERR_CONFIG, "max_ctas must be >= 0 (0 = all SMs)");
+    fy::set_max_ctas(max_ctas);
+    return FY_OK;
+}
+
 extern "C" fy_status fy_adamw_tune_bulk(int tile, int split, int probe) {
     if (tile != 1024 && tile != 2048 && tile != 4096) return fail(FY_ERR_CONFIG, "tile must be 1024, 2048 or 4096");
     if (split != 0 && split != 1) return fail(FY_ERR_CONFIG, "split must be 0 or 1");
