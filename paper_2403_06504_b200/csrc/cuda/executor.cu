@@ -726,16 +726,32 @@ MeasuredRates Engine::calibrate() {
         r.file_write_bps = bytes / best_w;
         r.file_read_bps = bytes / best_r;
         // effective: replay the graph's own file-lane operations in task
-        // order (each <= the probe size, <= 2 GiB in total) — reads and
-        // writes interleaved as the iteration issues them
+        // order (each <= the probe size, <= 8 GiB in total) — reads and
+        // writes interleaved as the iteration issues them, writes at a
+        // moving cursor over an 8 GiB region and reads cycling over what
+        // has been written, so a device / host cache cannot serve the
+        // replay from one hot 512 MiB region (r01an: a 2 GiB single-region
+        // replay predicted 5.6 GB/s where 75 GB of iteration IO got 4.0)
+        constexpr std::uint64_t kReplay = 8ull << 30;
         double rd_b = 0, rd_s = 0, wr_b = 0, wr_s = 0;
+        std::uint64_t wcur = round_up(bytes), written = round_up(bytes), rcur = 0;
         for (const Task& t : g_.tasks) {
             if (t.resource != ResourceId::link_ssd || t.work <= 0.0) continue;
-            if (rd_b + wr_b >= double(2ull << 30)) break;
+            if (rd_b + wr_b >= double(kReplay)) break;
             const std::uint64_t b = round_up(std::min<std::uint64_t>(static_cast<std::uint64_t>(t.work), bytes));
             IoRequest op = w;
             op.bytes = b;
             op.write = t.dir == TransferDir::c2s;
+            if (op.write) {
+                if (wcur + b > kReplay) wcur = 0;
+                op.offset = wcur;
+                wcur += b;
+                written = std::max(written, wcur);
+            } else {
+                if (rcur + b > written) rcur = 0;
+                op.offset = rcur;
+                rcur += b;
+            }
             const auto t0 = std::chrono::steady_clock::now();
             run_io(&op);
             const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
