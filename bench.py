@@ -1346,6 +1346,12 @@ def main():
     if "e2e" in res:
         e = dict(res["e2e"])
         e.pop("launches", None)
+        if pcie and pcie.get("duplex_each_gbs"):
+            # the e2e step is host-link bound: 2 B/param each way, both ways at once
+            e["roofline"] = {"bound": "host-link duplex (per direction)", "achieved": e["link_gbs_each_way"],
+                             "peak": pcie["duplex_each_gbs"], "unit": "GB/s",
+                             "frac": e["link_gbs_each_way"] / pcie["duplex_each_gbs"],
+                             "peak_source": "in-run pinned cudaMemcpyAsync, H2D+D2H concurrent (1 GiB)"}
         line["e2e"] = e
     if cpu is not None:
         line["cpu_baseline"] = cpu
