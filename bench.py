@@ -204,7 +204,7 @@ def barrier(world):
 
 # ------------------------------------------------------------ CPU baseline
 
-def cpu_oracle_rate(chunk: int, nchunks: int, target_s: float = 12.0, max_reps: int = 50):
+def cpu_oracle_rate(chunk: int, nchunks: int, target_s: float = 12.0, max_reps: int = 200):
     """Oracle port (DeepSpeed CPU Adam restatement) over all host threads on
     `nchunks` chunks of `chunk` params; returns (params/s, threads, sample)."""
     from oracle import oracle as O
