@@ -160,7 +160,8 @@ fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
  * (3 stages x 2048 only): 1 = L2 evict_first cache hints on the bulk
  * copies; 2 = the same traffic with the arithmetic skipped (states written
  * back unchanged: a speed-of-light measurement, not an optimizer step);
- * 3 = both. 0 = off (default). */
+ * 3 = both; 4 = the DMA thread computing tile addresses before (not after)
+ * waiting for each stage (measured slower). 0 = off (default). */
 fy_status fy_adamw_tune_bulk(int tile, int split, int probe);
 /* SM budget of the fused step (TMA path), process-wide: launches use at most
  * max_ctas CTAs — one per SM — leaving the other SMs to a backward running

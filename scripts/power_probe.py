@@ -37,8 +37,14 @@ def step():
                       workspace=ws)
 
 
-for name, tune, bulk in (("tma_default", (1, 3, 0), (2048, 0, 0)), ("tma_no_arithmetic", (1, 3, 0), (2048, 0, 2)),
-                         ("lsu_unroll2", (0, 2, 2), (2048, 0, 0)), ("tma_default_again", (1, 3, 0), (2048, 0, 0))):
+VARIANTS = {
+    "default": (("tma_default", (1, 3, 0), (2048, 0, 0)), ("tma_no_arithmetic", (1, 3, 0), (2048, 0, 2)),
+                ("lsu_unroll2", (0, 2, 2), (2048, 0, 0)), ("tma_default_again", (1, 3, 0), (2048, 0, 0))),
+    # DMA thread computing addresses after (product) vs before (probe 4) each stage wait
+    "hoist": (("tma_after_wait", (1, 3, 0), (2048, 0, 0)), ("tma_hoisted", (1, 3, 0), (2048, 0, 4)),
+              ("tma_after_wait_2", (1, 3, 0), (2048, 0, 0)), ("tma_hoisted_2", (1, 3, 0), (2048, 0, 4))),
+}
+for name, tune, bulk in VARIANTS[sys.argv[1] if len(sys.argv) > 1 else "default"]:
     check(LIB.fy_adamw_tune(*tune))
     check(LIB.fy_adamw_tune_bulk(*bulk))
     step()
