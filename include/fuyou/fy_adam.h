@@ -161,7 +161,9 @@ fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
  * copies; 2 = the same traffic with the arithmetic skipped (states written
  * back unchanged: a speed-of-light measurement, not an optimizer step);
  * 3 = both; 4 = the DMA thread computing tile addresses before (not after)
- * waiting for each stage (measured slower). 0 = off (default). */
+ * waiting for each stage (measured slower); 5 / 6 = refilling the previous
+ * tile's stage instead of the one just stored (3 / 4 stages). 0 = off
+ * (default). */
 fy_status fy_adamw_tune_bulk(int tile, int split, int probe);
 /* SM budget of the fused step (TMA path), process-wide: launches use at most
  * max_ctas CTAs — one per SM — leaving the other SMs to a backward running

@@ -441,7 +441,7 @@ extern "C" fy_status fy_adamw_sm_budget(int max_ctas) {
 extern "C" fy_status fy_adamw_tune_bulk(int tile, int split, int probe) {
     if (tile != 1024 && tile != 2048 && tile != 4096) return fail(FY_ERR_CONFIG, "tile must be 1024, 2048 or 4096");
     if (split != 0 && split != 1) return fail(FY_ERR_CONFIG, "split must be 0 or 1");
-    if (probe < 0 || probe > 4) return fail(FY_ERR_CONFIG, "probe must be 0..4");
+    if (probe < 0 || probe > 6) return fail(FY_ERR_CONFIG, "probe must be 0..6");
     fy::set_bulk_variant(tile, split, probe);
     return FY_OK;
 }

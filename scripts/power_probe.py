@@ -43,6 +43,10 @@ VARIANTS = {
     # DMA thread computing addresses after (product) vs before (probe 4) each stage wait
     "hoist": (("tma_after_wait", (1, 3, 0), (2048, 0, 0)), ("tma_hoisted", (1, 3, 0), (2048, 0, 4)),
               ("tma_after_wait_2", (1, 3, 0), (2048, 0, 0)), ("tma_hoisted_2", (1, 3, 0), (2048, 0, 4))),
+    # refill the previous tile's stage (wait_group.read 1) vs the one just stored
+    "lag": (("tma_default", (1, 3, 0), (2048, 0, 0)), ("lag_3stages", (1, 3, 0), (2048, 0, 5)),
+            ("lag_4stages", (1, 3, 0), (2048, 0, 6)), ("tma_default_2", (1, 3, 0), (2048, 0, 0)),
+            ("lag_3stages_2", (1, 3, 0), (2048, 0, 5)), ("lag_4stages_2", (1, 3, 0), (2048, 0, 6))),
 }
 for name, tune, bulk in VARIANTS[sys.argv[1] if len(sys.argv) > 1 else "default"]:
     check(LIB.fy_adamw_tune(*tune))
