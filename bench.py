@@ -25,6 +25,15 @@ buffer becomes the updated bf16 params, task_graph.cpp:493-495).
            mean launch time (CUDA events) vs MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline: the CPU restatement (oracle/, OpenMP over all host threads)
            on a bounded sample of the same chunks.
+  also:    multi_chunk_step (the same step as one fy_adamw_chunks call),
+           configs (C1 eager / CUDA graph / multi-chunk / streamed; one C4
+           175B block resident, per-rank shard slices, streamed),
+           streamed_shard (175B-shaped blocks sharded across ranks, streamed
+           from NUMA-local pinned memory, N>1 all-gathers overlapped),
+           executed_iteration (offsim_execute: C1 b8 / b128 and a 13B slice
+           with real GEMMs feeding the optimizer's gradients; executed vs
+           predicted), swap_sweep (BASELINE config 5 through the planner),
+           swap_engine (fy_swapper_* GB/s), b200_replanning.
 
 N>1 (torchrun): every chunk is sharded across ranks (fy_shard_range, 8-elem
 aligned slices); each rank updates its slice; the updated bf16 slices reach
