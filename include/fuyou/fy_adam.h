@@ -97,7 +97,9 @@ typedef struct fy_adamw_args {
     /* Optional device-side controls (enqueue-only clipping / overflow skip;
      * see fy_clip_coef). NULL = off. */
     const float* grad_scale_dev; /* effective scale = fl(hp.grad_scale * *grad_scale_dev) */
-    const int* skip_if_set;      /* *skip_if_set != 0: the launch writes nothing      */
+    const int* skip_if_set;      /* *skip_if_set != 0: states untouched, params
+                                    rewritten from the unchanged master (the
+                                    param buffer may alias this step's grads) */
 } fy_adamw_args;
 
 uint32_t fy_adamw_workspace_floats(void);
@@ -248,6 +250,12 @@ void fy_pipeline_destroy(fy_pipeline* p);
 fy_status fy_pipeline_step(fy_pipeline* p, const fy_chunk* chunks, uint32_t count,
                            const fy_adam_hparams* hp, int want_grad_norm);
 fy_status fy_pipeline_wait(fy_pipeline* p, double* grad_sq_sum, int* nonfinite);
+
+/* Device-side clip coefficient / overflow-skip flag (fy_clip_coef outputs)
+ * applied by the following steps' updates (NULL = off). A skipped update
+ * leaves the states unchanged and still writes the params (from the
+ * unchanged master), so the write-backs stay correct. */
+fy_status fy_pipeline_set_controls(fy_pipeline* p, const float* grad_scale_dev, const int* skip_if_set);
 
 /* Timings of the last completed step (count entries). */
 fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32_t count,

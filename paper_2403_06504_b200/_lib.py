@@ -101,6 +101,7 @@ def _load() -> C.CDLL:
         "fy_adamw_sm_budget": (st, [C.c_int]),
         "fy_adamw_chunks": (st, [C.POINTER(AdamwArgs), C.c_uint32, C.c_void_p]),
         "fy_clip_coef": (st, [C.c_void_p, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "fy_pipeline_set_controls": (st, [C.c_void_p, C.c_void_p, C.c_void_p]),
         "fy_device_info": (st, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]),
         "fy_shard_range": (st, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,

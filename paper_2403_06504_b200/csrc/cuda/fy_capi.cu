@@ -269,6 +269,12 @@ fy_status fy_pipeline_wait(fy_pipeline* p, double* grad_sq_sum, int* nonfinite) 
     });
 }
 
+fy_status fy_pipeline_set_controls(fy_pipeline* p, const float* grad_scale_dev, const int* skip_if_set) {
+    if (!p) return fail(FY_ERR_CONFIG, "null argument");
+    p->impl.set_controls(grad_scale_dev, skip_if_set);
+    return FY_OK;
+}
+
 fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32_t count,
                               uint64_t* step_ns) {
     if (!p || (!out && count > 0)) return fail(FY_ERR_CONFIG, "null argument");

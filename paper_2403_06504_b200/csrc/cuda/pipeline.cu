@@ -227,6 +227,8 @@ void ChunkPipeline::step(const fy_chunk* chunks, std::uint32_t count, const fy_a
     want_norm_ = want_norm;
     scalars_ = make_scalars(hp.lr, hp.beta1, hp.beta2, hp.eps, hp.weight_decay, hp.step,
                             hp.adamw_mode, hp.bias_correction, hp.grad_scale);
+    scalars_.scale_dev = scale_dev_;  // a skipped update still writes params from master
+    scalars_.skip_dev = skip_dev_;
 
     // Step boundary: the previous step's write-backs own the slots.
     if (have_prev_) check_cuda(cudaStreamWaitEvent(h2d_, step_end_, 0), "wait prev");

@@ -43,6 +43,12 @@ public:
               bool want_norm);
     void wait(double* grad_sq_sum, int* nonfinite);
     void timings(fy_chunk_timing* out, std::uint32_t count, std::uint64_t* step_ns) const;
+    // device-side clip coefficient / overflow-skip flag for the following
+    // steps (fy_clip_coef outputs; nullptr = off)
+    void set_controls(const float* scale_dev, const int* skip_dev) {
+        scale_dev_ = scale_dev;
+        skip_dev_ = skip_dev;
+    }
 
     cudaStream_t h2d_stream() const { return h2d_; }
     cudaStream_t d2h_stream() const { return d2h_; }
@@ -76,6 +82,8 @@ private:
     // Current step's inputs (valid during step()).
     const fy_chunk* chunks_ = nullptr;
     AdamScalars scalars_{};
+    const float* scale_dev_ = nullptr;
+    const int* skip_dev_ = nullptr;
 };
 
 } // namespace fy

@@ -199,6 +199,12 @@ class ChunkPipeline:
         self._chunks = arr  # keep alive until wait()
         check(LIB.fy_pipeline_step(self._h, arr, len(chunks), C.byref(hp.c()), int(want_grad_norm)))
 
+    def set_controls(self, grad_scale_dev: Optional[torch.Tensor] = None,
+                     skip_if_set: Optional[torch.Tensor] = None) -> None:
+        """fy_pipeline_set_controls: device-side clip coefficient / skip flag."""
+        check(LIB.fy_pipeline_set_controls(self._h, C.c_void_p(_ptr(grad_scale_dev)),
+                                           C.c_void_p(_ptr(skip_if_set))))
+
     def wait(self):
         sq, bad = C.c_double(), C.c_int()
         check(LIB.fy_pipeline_wait(self._h, C.byref(sq), C.byref(bad)))

@@ -254,3 +254,45 @@ def test_pipeline_update_done_events(cuda_dev):
         O.adamw_step(st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy(), r["grad"], O.BF16, sc, param_out=op)
         assert np.array_equal(s.cpu().view(torch.int16).numpy().view(np.uint16), op)
     pipe.close()
+
+
+@pytest.mark.parametrize("overflow", [False, True])
+def test_pipeline_device_side_clip_and_skip(cuda_dev, overflow):
+    """Streamed step with enqueue-only clipping / overflow skip
+    (fy_pipeline_set_controls + fy_clip_coef): clipped updates are bit-exact
+    vs the oracle with the combined scale; a skipped step writes the
+    unchanged states back and bf16(master) as params."""
+    from paper_2403_06504_b200 import optim as F
+    sizes = [1 << 20, 4099, (1 << 19) + 8]
+    chunks, ref = _make_chunks(sizes, 41, cuda_dev, grads_on_host=False)
+    if overflow:
+        chunks[1]["grad_t"][7] = float("inf")
+        ref[1]["grad"][7] = 0x7F80
+    ws = torch.zeros(F.workspace_floats(), device=cuda_dev)
+    sq = torch.zeros(1, dtype=torch.float64, device=cuda_dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=cuda_dev)
+    coef = torch.zeros(1, dtype=torch.float32, device=cuda_dev)
+    skip = torch.zeros(1, dtype=torch.int32, device=cuda_dev)
+    for k, c in enumerate(chunks):
+        F.grad_stats(c["grad_t"], 1.0, sq, ws, nonfinite=bad, accumulate=k > 0)
+    F.clip_coef(sq, bad, 1e-3, coef, skip)
+    pipe = F.ChunkPipeline(max(sizes), slots=2)
+    pipe.set_controls(coef, skip)
+    pipe.step(_desc(chunks), F.Hparams(step=10))
+    pipe.wait()
+    torch.cuda.synchronize()
+    assert int(skip.item()) == int(overflow)
+    c_val = float(coef.item())
+    for c, r in zip(chunks, ref):
+        n = r["grad"].size
+        st = r["states"]
+        mst, mm, vv = st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()
+        if overflow:
+            want_p = torch.from_numpy(mst).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        else:
+            want_p = np.zeros(n, np.uint16)
+            O.adamw_step(mst, mm, vv, r["grad"], O.BF16, O.scalars(step=10),
+                         grad_scale=float(np.float32(1.0) * np.float32(c_val)), param_out=want_p)
+        assert _bits_equal(c["h_states_t"].numpy(), np.concatenate([mst, mm, vv]))
+        assert np.array_equal(c["h_param_t"].view(torch.int16).numpy().view(np.uint16), want_p)
+    pipe.close()
