@@ -651,6 +651,9 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
     import torch.distributed as dist
     L = len(states)
     n = slice_pad
+    # the link's duplex rate right before this phase (host links drift over a
+    # run): the denominator of the e2e roofline
+    link_now = pcie_peaks(torch) if world == 1 else None
     if world > 1 and full is None:  # IPC-gather runs keep no torch-side full buffers
         full = [torch.empty(world * n, dtype=torch.bfloat16, device="cuda") for _ in range(L)]
     hbuf = []
@@ -712,6 +715,7 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
                 + ("; + in-place NCCL all-gather of the device-side bf16 slices" if world > 1 else ""),
         "launches": args.steps * len(chunks) * 2,
         "pieces_per_block": len(spans),
+        "pcie_at_e2e": link_now,
     }
 
 
@@ -1355,12 +1359,14 @@ def main():
     if "e2e" in res:
         e = dict(res["e2e"])
         e.pop("launches", None)
-        if pcie and pcie.get("duplex_each_gbs"):
+        link = e.get("pcie_at_e2e") or pcie
+        if link and link.get("duplex_each_gbs"):
             # the e2e step is host-link bound: 2 B/param each way, both ways at once
             e["roofline"] = {"bound": "host-link duplex (per direction)", "achieved": e["link_gbs_each_way"],
-                             "peak": pcie["duplex_each_gbs"], "unit": "GB/s",
-                             "frac": e["link_gbs_each_way"] / pcie["duplex_each_gbs"],
-                             "peak_source": "in-run pinned cudaMemcpyAsync, H2D+D2H concurrent (1 GiB)"}
+                             "peak": link["duplex_each_gbs"], "unit": "GB/s",
+                             "frac": e["link_gbs_each_way"] / link["duplex_each_gbs"],
+                             "peak_source": "pinned cudaMemcpyAsync, H2D+D2H concurrent (1 GiB), "
+                                            "measured right before the e2e phase"}
         line["e2e"] = e
     if cpu is not None:
         line["cpu_baseline"] = cpu
