@@ -230,7 +230,13 @@ typedef struct fy_chunk {
                              chunk's update (e.g. to start its all-gather
                              on another stream while the next chunks are
                              still streaming)                            */
+    uint32_t flags;       /* FY_CHUNK_STATES_ON_DEVICE: this chunk's
+                             h_states is DEVICE memory kept resident in HBM
+                             (no state copies; params still go to h_param) —
+                             lets spare HBM hold part of an out-of-core
+                             model's optimizer states                   */
 } fy_chunk;
+#define FY_CHUNK_STATES_ON_DEVICE 1u
 
 /* Per-chunk timings of the last step, in ns relative to the step start
  * (CUDA events): h2d [start,end), update [start,end), d2h [start,end). */

@@ -58,7 +58,7 @@ class Chunk(C.Structure):
     _fields_ = [
         ("n", C.c_uint64), ("h_states", C.c_void_p), ("grad", C.c_void_p),
         ("h_param", C.c_void_p), ("d_param", C.c_void_p), ("grad_ready", C.c_void_p),
-        ("states_stride", C.c_uint64), ("update_done", C.c_void_p),
+        ("states_stride", C.c_uint64), ("update_done", C.c_void_p), ("flags", C.c_uint32),
     ]
 
 
@@ -70,6 +70,7 @@ class SwapConfig(C.Structure):
 
 
 FY_SWAP_CPU, FY_SWAP_SSD = 0, 1
+FY_CHUNK_STATES_ON_DEVICE = 1
 
 
 class ChunkTiming(C.Structure):

@@ -299,6 +299,9 @@ fy_status fy_graph_execute(const char* scenario_json, const char* exec_opts_json
             if (chunks[k].n != 12ull * sc.model.hidden_dim * sc.model.hidden_dim)
                 throw offsim::ConfigError("fy_graph_execute: chunk " + std::to_string(k) +
                                           " size differs from 12*h^2");
+            if (chunks[k].flags != 0)
+                throw offsim::ConfigError("fy_graph_execute: chunk " + std::to_string(k) +
+                                          ": chunk flags are a pipeline feature");
             if (chunks[k].states_stride != 0 && chunks[k].states_stride != chunks[k].n)
                 throw offsim::ConfigError("fy_graph_execute: chunk " + std::to_string(k) +
                                           ": strided states are a pipeline feature (contiguous here)");

@@ -128,7 +128,7 @@ void ChunkPipeline::issue_h2d(std::uint32_t i) {
     if (i >= S) check_cuda(cudaStreamWaitEvent(h2d_, ev(i - S, kD2hEnd), 0), "wait slot");
     if (i >= 2) check_cuda(cudaStreamWaitEvent(h2d_, ev(i - 2, kUpdEnd), 0), "wait read gate");
     check_cuda(cudaEventRecord(ev(i, kH2dStart), h2d_), "record");
-    if (!cfg_.states_on_device) {
+    if (!resident(c)) {
         const std::uint64_t stride = c.states_stride ? c.states_stride : c.n;
         if (stride == c.n)
             check_cuda(cudaMemcpyAsync(slot.states, c.h_states, 12ull * c.n, cudaMemcpyHostToDevice,
@@ -158,9 +158,9 @@ void ChunkPipeline::issue_update(std::uint32_t i) {
                    "wait grad");
     check_cuda(cudaEventRecord(ev(i, kUpdStart), opt_), "record");
     AdamLaunch a{};
-    float* states = reinterpret_cast<float*>(cfg_.states_on_device ? c.h_states : slot.states);
+    float* states = reinterpret_cast<float*>(resident(c) ? c.h_states : slot.states);
     // staged slots are contiguous; device-resident states keep the caller's stride
-    const std::uint64_t stride = cfg_.states_on_device && c.states_stride ? c.states_stride : c.n;
+    const std::uint64_t stride = resident(c) && c.states_stride ? c.states_stride : c.n;
     a.master = states;
     a.m = states + stride;
     a.v = states + 2 * stride;
@@ -185,7 +185,7 @@ void ChunkPipeline::issue_d2h(std::uint32_t i) {
     Slot& slot = slots_[i % slots_.size()];
     check_cuda(cudaStreamWaitEvent(d2h_, ev(i, kUpdEnd), 0), "wait update");
     check_cuda(cudaEventRecord(ev(i, kD2hStart), d2h_), "record");
-    if (!cfg_.states_on_device) {
+    if (!resident(c)) {
         const std::uint64_t stride = c.states_stride ? c.states_stride : c.n;
         if (stride == c.n)
             check_cuda(cudaMemcpyAsync(c.h_states, slot.states, 12ull * c.n, cudaMemcpyDeviceToHost,

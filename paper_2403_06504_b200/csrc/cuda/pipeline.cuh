@@ -58,6 +58,11 @@ private:
     enum Ev { kH2dStart, kH2dEnd, kUpdStart, kUpdEnd, kD2hStart, kD2hEnd, kEvPerChunk };
     cudaEvent_t ev(std::uint32_t chunk, int which) const { return events_[chunk * kEvPerChunk + which]; }
     void ensure_events(std::uint32_t count);
+    // states of this chunk live in device memory (the whole pipeline's
+    // states_on_device, or the chunk's FY_CHUNK_STATES_ON_DEVICE flag)
+    bool resident(const fy_chunk& c) const {
+        return cfg_.states_on_device || (c.flags & FY_CHUNK_STATES_ON_DEVICE) != 0;
+    }
     void issue_h2d(std::uint32_t i);
     void issue_update(std::uint32_t i);
     void issue_d2h(std::uint32_t i);

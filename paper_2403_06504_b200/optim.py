@@ -195,7 +195,8 @@ class ChunkPipeline:
         arr = (Chunk * len(chunks))()
         for i, c in enumerate(chunks):
             arr[i] = Chunk(c["n"], c["h_states"], c["grad"], c.get("h_param"), c.get("d_param"),
-                           c.get("grad_ready"), c.get("states_stride", 0), c.get("update_done"))
+                           c.get("grad_ready"), c.get("states_stride", 0), c.get("update_done"),
+                           c.get("flags", 0))
         self._chunks = arr  # keep alive until wait()
         check(LIB.fy_pipeline_step(self._h, arr, len(chunks), C.byref(hp.c()), int(want_grad_norm)))
 

@@ -51,7 +51,7 @@ def graph_execute(scenario: str, opts: dict, chunks):
     L = lib()
     arr = (Chunk * len(chunks))()
     for i, c in enumerate(chunks):
-        arr[i] = Chunk(c["n"], c["h_states"], c["grad"], c["h_param"], None, None, 0, None)
+        arr[i] = Chunk(c["n"], c["h_states"], c["grad"], c["h_param"], None, None, 0, None, 0)
     summ = C.c_void_p()
     st = L.fy_graph_execute(scenario.encode(), json.dumps(opts).encode(), arr, len(chunks),
                             C.byref(summ))

@@ -296,3 +296,36 @@ def test_pipeline_device_side_clip_and_skip(cuda_dev, overflow):
         assert _bits_equal(c["h_states_t"].numpy(), np.concatenate([mst, mm, vv]))
         assert np.array_equal(c["h_param_t"].view(torch.int16).numpy().view(np.uint16), want_p)
     pipe.close()
+
+
+def test_pipeline_mixed_resident_and_streamed_chunks(cuda_dev):
+    """FY_CHUNK_STATES_ON_DEVICE: chunks whose states stay in HBM (spare HBM
+    holding part of an out-of-core model's states) mixed with streamed ones
+    in one step; all bit-exact vs the oracle, resident states updated in
+    place on the device, every chunk's params written to host."""
+    from paper_2403_06504_b200 import optim as F
+    from paper_2403_06504_b200._lib import FY_CHUNK_STATES_ON_DEVICE
+    sizes = [1 << 20, (1 << 20) + 8, 4099, 1 << 19]
+    chunks, ref = _make_chunks(sizes, 51, cuda_dev, grads_on_host=False)
+    resident = {0, 2}
+    dev_states = {k: chunks[k]["h_states_t"].to(cuda_dev) for k in resident}
+    desc = _desc(chunks)
+    for k in resident:
+        desc[k]["h_states"] = dev_states[k].data_ptr()
+        desc[k]["flags"] = FY_CHUNK_STATES_ON_DEVICE
+    pipe = F.ChunkPipeline(max(sizes), slots=2)
+    for step in (10, 11):
+        pipe.step(desc, F.Hparams(step=step))
+        pipe.wait()
+        sc = O.scalars(step=step)
+        for k, (c, r) in enumerate(zip(chunks, ref)):
+            n = r["grad"].size
+            st = r["states"]
+            mst, mm, vv = st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()
+            op = np.zeros(n, np.uint16)
+            O.adamw_step(mst, mm, vv, r["grad"], O.BF16, sc, param_out=op)
+            r["states"] = np.concatenate([mst, mm, vv])
+            got = dev_states[k].cpu().numpy() if k in resident else c["h_states_t"].numpy()
+            assert _bits_equal(got, r["states"]), f"chunk {k} step {step}"
+            assert np.array_equal(c["h_param_t"].view(torch.int16).numpy().view(np.uint16), op)
+    pipe.close()
