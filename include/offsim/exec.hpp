@@ -93,6 +93,9 @@ struct ExecOptions {
     bool host_ring_auto = false;
     // Report an FNV-1a checksum of every chunk's final [master|m|v].
     bool checksum_states = false;
+    // Optimizer groups g0..g(R-1) whose states stay resident in HBM (see
+    // map_graph_for_b200); 0xffffffff = all groups ("all").
+    std::uint32_t resident_groups = 0;
 };
 
 // Caller-provided optimizer states for chunk (block) k: pinned host
@@ -108,8 +111,12 @@ struct ChunkBuffers {
 // counts for transfers that do not physically happen on B200 under `tier`.
 // The m-th optimizer group (processing order) stages its states in device
 // slot m % state_slots; the slot-reuse edge is part of the mapped graph.
+// resident_groups: optimizer groups g0 .. g(R-1) keep master / m / v in HBM
+// for the whole run (B200's HBM holds what the schedule leaves free): their
+// state_h2d / state_d2h (and, file tier, state_s2c / state_c2s) move 0 B and
+// their 12N B are booked in the GPU pool from the start (initial_mem).
 TaskGraph map_graph_for_b200(const TaskGraph& graph, StateTier tier,
-                             std::uint32_t state_slots = 3);
+                             std::uint32_t state_slots = 3, std::uint32_t resident_groups = 0);
 
 // Slot-reuse edges of the bounded host staging rings (file tier): the n-th
 // use of a ring waits for the last task of use n - slots. Uses are, in task

@@ -42,7 +42,8 @@ ParsedOptions parse_options(const char* text) {
                                                "compute_rate", "state_slots", "seed",
                                                "verify_swaps", "adam", "dry_run", "variant",
                                                "swap_only", "max_blocks", "placement",
-                                               "compute_mode", "host_ring", "checksum_states"};
+                                               "compute_mode", "host_ring", "checksum_states",
+                                               "resident_groups"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -69,6 +70,13 @@ ParsedOptions parse_options(const char* text) {
             o.host_ring = doc.value("host_ring", o.host_ring);
         }
         o.checksum_states = doc.value("checksum_states", o.checksum_states);
+        if (doc.contains("resident_groups") && doc.at("resident_groups").is_string()) {
+            if (doc.at("resident_groups").get<std::string>() != "all")
+                throw ConfigError("exec options: resident_groups must be a count or 'all'");
+            o.resident_groups = 0xffffffffu;
+        } else {
+            o.resident_groups = doc.value("resident_groups", o.resident_groups);
+        }
         o.swap_only = doc.value("swap_only", o.swap_only);
         o.max_blocks = doc.value("max_blocks", o.max_blocks);
         out.placement = doc.value("placement", out.placement);
@@ -204,7 +212,7 @@ SwapPlan plan_with_placement(const Scenario& s, const std::string& placement) {
 std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVariant v) {
     const SwapPlan plan = plan_with_placement(s, po.placement);
     const TaskGraph ref = build_schedule(s.model, s.hardware, plan, v);
-    TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots);
+    TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots, po.exec.resident_groups);
     if (po.exec.swap_only) mapped = swap_subgraph(mapped, po.exec.max_blocks);
     const RingDepths rings = host_ring_depths(mapped, po.exec);
     add_host_ring_edges(mapped, rings);

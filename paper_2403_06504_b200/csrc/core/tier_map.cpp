@@ -38,7 +38,8 @@ std::string group_of(const std::string& name) { return name.substr(name.rfind(' 
 
 } // namespace
 
-TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t state_slots) {
+TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t state_slots,
+                             std::uint32_t resident_groups) {
     if (state_slots < 2) throw ConfigError("executor: state_slots must be >= 2");
     const bool overlapped = in.header.variant == ScheduleVariant::overlapped;
     if (!overlapped && tier == StateTier::host)
@@ -83,6 +84,13 @@ TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t 
         if (starts_with(t.name, "opt state_s2c ")) state_bytes[group_of(t.name)] = t.work;
         if (starts_with(t.name, "opt param_c2s ")) param_bytes[group_of(t.name)] = t.work;
     }
+    // groups "g0".."g(R-1)" keep their states in HBM for the whole run
+    auto resident = [&](const std::string& g) {
+        return resident_groups > 0 && g.size() > 1 && g[0] == 'g' &&
+               std::stoul(g.substr(1)) < resident_groups;
+    };
+    for (const auto& [g, sb] : state_bytes)
+        if (resident(g)) out.initial_mem[ResourceId::mem_gpu] += static_cast<std::int64_t>(sb);
 
     for (const Task& src : in.tasks) {
         Task t = src;
@@ -91,6 +99,10 @@ TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t 
         const auto i64 = [](double b) { return static_cast<std::int64_t>(b); };
 
         if (t.resource == ResourceId::link_ssd && tier == StateTier::host) t.work = 0.0;
+        if ((starts_with(src.name, "opt state_s2c ") || starts_with(src.name, "opt state_c2s ")) && resident(g)) {
+            t.work = 0.0;  // resident states never leave HBM
+            t.mem_effects.clear();
+        }
 
         if (starts_with(src.name, "bwd grad_g2c ") && overlapped) {
             // gradients stay in HBM and feed the fused kernel directly
@@ -118,17 +130,20 @@ TaskGraph map_graph_for_b200(const TaskGraph& in, StateTier tier, std::uint32_t 
             std::vector<std::uint32_t> h2d_deps{state_read};
             if (d2h_in_order.size() >= state_slots)
                 h2d_deps.push_back(d2h_in_order[d2h_in_order.size() - state_slots]);
+            const bool res = resident(g);
             h2d_of[g] = hop("opt state_h2d " + g, ResourceId::link_c2g, TransferDir::c2g,
-                            Payload::opt_states, sb, std::move(h2d_deps),
-                            {MemEffect{ResourceId::mem_gpu, i64(sb), true}});
+                            Payload::opt_states, res ? 0.0 : sb, std::move(h2d_deps),
+                            res ? std::vector<MemEffect>{}
+                                : std::vector<MemEffect>{MemEffect{ResourceId::mem_gpu, i64(sb), true}});
             t.deps.push_back(h2d_of[g]);
             t.mem_effects.clear();
             const std::uint32_t upd = push(std::move(t));
             remap[src.id] = upd;
             const double pb = param_bytes[g];
             d2h_of[g] = hop("opt state_d2h " + g, ResourceId::link_g2c, TransferDir::g2c,
-                            Payload::opt_states, sb, {upd},
-                            {MemEffect{ResourceId::mem_gpu, -i64(sb), false}});
+                            Payload::opt_states, res ? 0.0 : sb, {upd},
+                            res ? std::vector<MemEffect>{}
+                                : std::vector<MemEffect>{MemEffect{ResourceId::mem_gpu, -i64(sb), false}});
             d2h_in_order.push_back(d2h_of[g]);
             pd2h_of[g] = hop("opt param_d2h " + g, ResourceId::link_g2c, TransferDir::g2c,
                              Payload::params, pb, {upd},

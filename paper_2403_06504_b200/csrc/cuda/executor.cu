@@ -314,6 +314,11 @@ private:
     std::vector<void*> h_states_, h_params_;
     // device side
     std::vector<Device> own_grads_, act_dev_, act_restore_, ckpt_dev_, ckpt_restore_, slots_;
+    std::vector<Device> res_states_;  // resident optimizer groups g0..g(R-1): states in HBM
+    std::uint32_t resident_ = 0;
+    bool is_resident(std::uint32_t k) const { return k < resident_; }
+    void* read_tier_states(std::uint32_t k, Pinned& tmp);  // initial states of chunk k
+    void write_back_resident();                             // after the run
     std::vector<const void*> d_grads_;
     Device wscratch_[2];
     int wscratch_turn_ = 0;
@@ -594,6 +599,15 @@ void Engine::setup() {
         }
         if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
     }
+    if (has_update_ && opt_.resident_groups > 0) {
+        resident_ = std::min<std::uint32_t>(opt_.resident_groups, blocks_);
+        Pinned tmp;
+        for (std::uint32_t k = 0; k < resident_; ++k) {
+            res_states_.emplace_back(state_b);
+            check_cuda(cudaMemcpy(res_states_.back().p, read_tier_states(k, tmp), state_b, cudaMemcpyHostToDevice),
+                       "resident states");
+        }
+    }
     const AdamHyper& a = opt_.adam;
     scalars_ = fy::make_scalars(a.lr, a.beta1, a.beta2, a.eps, a.weight_decay, a.step,
                                 a.adamw_mode, a.bias_correction, a.grad_scale);
@@ -823,6 +837,40 @@ void Engine::assign_ring_slots() {
     }
 }
 
+// Initial [master|m|v] of chunk k from its tier: the pinned host copy, or
+// (file tier with staging rings) a read of its file region into `tmp`.
+void* Engine::read_tier_states(std::uint32_t k, Pinned& tmp) {
+    const std::uint64_t state_b = 12 * n_;
+    if (h_states_[k]) return h_states_[k];  // the host copy the tier was seeded from
+    if (!tmp.p) tmp = Pinned(round_up(state_b));
+    IoRequest r{&io_, f_states_->fd(), tmp.p, round_up(state_b), k * round_up(state_b), false, false,
+                &io_error_, &io_error_text_, &io_mu_};
+    run_io(&r);
+    if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
+    return tmp.p;
+}
+
+// Resident groups' final states go back to their tier after the run (host
+// copy and/or file region), so checksums and caller buffers see them.
+void Engine::write_back_resident() {
+    const std::uint64_t state_b = 12 * n_;
+    Pinned tmp;
+    for (std::uint32_t k = 0; k < resident_; ++k) {
+        void* dst = h_states_[k];
+        if (!dst) {
+            if (!tmp.p) tmp = Pinned(round_up(state_b));
+            dst = tmp.p;
+        }
+        check_cuda(cudaMemcpy(dst, res_states_[k].p, state_b, cudaMemcpyDeviceToHost), "resident write-back");
+        if (file_tier_) {
+            IoRequest w{&io_, f_states_->fd(), dst, round_up(state_b), k * round_up(state_b), true, false,
+                        &io_error_, &io_error_text_, &io_mu_};
+            run_io(&w);
+        }
+    }
+    if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
+}
+
 // FNV-1a over 64-bit words of every chunk's final [master|m|v], read back
 // from the file tier (or the pinned host copies) after the run.
 std::uint64_t Engine::checksum_states() {
@@ -927,7 +975,7 @@ void Engine::issue(const Task& t, ExecReport& rep) {
     } else if (t.kind == TaskKind::optimizer_update) {
         const int slot = slot_of(k);
         fy::AdamLaunch l{};
-        l.master = static_cast<float*>(slots_[slot].p);
+        l.master = static_cast<float*>(is_resident(k) ? res_states_[k].p : slots_[slot].p);
         l.m = l.master + n_;
         l.v = l.master + 2 * n_;
         l.grad = d_grads_[k];
@@ -1031,6 +1079,7 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
     check_cuda(cudaMemcpy(&rep.grad_sq_sum, d_norm_.p, sizeof(double), cudaMemcpyDeviceToHost), "norm");
     rep.expected_grad_sq_sum = dataflow_ ? expected_grad_sq_ : -1.0;
     rep.pinned_host_bytes = pinned_bytes_;
+    if (resident_ > 0) write_back_resident();
     if (opt_.checksum_states && has_update_) rep.state_checksum = checksum_states();
     check_cuda(cudaMemcpy(&rep.nonfinite, d_bad_.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
 
@@ -1078,7 +1127,8 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
                    const std::vector<ChunkBuffers>* chunks) {
     ExecReport rep;
     TaskGraph reference = build_schedule(model, hw, plan, variant);
-    rep.graph = map_graph_for_b200(reference, options.tier, std::max<std::uint32_t>(2, options.state_slots));
+    rep.graph = map_graph_for_b200(reference, options.tier, std::max<std::uint32_t>(2, options.state_slots),
+                                   options.resident_groups);
     if (options.swap_only) {
         reference = swap_subgraph(reference, options.max_blocks);
         rep.graph = swap_subgraph(rep.graph, options.max_blocks);

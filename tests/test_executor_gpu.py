@@ -197,3 +197,24 @@ def test_gemm_dataflow_grads_feed_the_optimizer(cuda_dev):
     st2, summ2, _, err2 = execute(sc, {"tier": "host", "compute_mode": "gemm"})
     assert st2 == 0, err2
     assert abs(summ2["optimizer"]["grad_sq_sum"] - exp) > 1e-3 * exp
+
+
+@pytest.mark.parametrize("tier", ["host", "file"])
+def test_resident_groups_same_states_fewer_bytes(cuda_dev, tmp_path, tier):
+    """resident_groups keeps g0..g2's optimizer states in HBM for the run:
+    the final states (checksum over every chunk, written back to the tier)
+    equal those of the all-streamed run bit for bit, the state bytes moved
+    drop by 2 x 12N per resident group, and the invariants hold."""
+    sc = scenario(layers=6, batch=2, seq=512)
+    base = {"tier": tier, "checksum_states": True, "seed": 7}
+    if tier == "file":
+        base.update(file_dir=str(tmp_path))
+    st0, s0, _, e0 = execute(sc, base)
+    st1, s1, _, e1 = execute(sc, {**base, "resident_groups": 3})
+    assert st0 == 0 and st1 == 0, (e0, e1)
+    assert s1["all_invariants_pass"], s1["invariants"]
+    assert s1["state_checksum"] == s0["state_checksum"] != 0
+    n = 12 * 768 * 768
+    pb0, pb1 = s0["physical_bytes"], s1["physical_bytes"]
+    assert pb1["h2d/opt_states"] == pb0["h2d/opt_states"] - 3 * 12 * n
+    assert pb1["d2h/opt_states"] == pb0["d2h/opt_states"] - 3 * 12 * n

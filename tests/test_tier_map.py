@@ -116,3 +116,29 @@ def test_host_ring_auto_follows_reference_windows():
     assert s0["host_ring"] == {"states": 0, "params": 0, "weights": 0, "acts": 0}
     st, _, _, err = execute(C1_SSD, {"dry_run": True, "tier": "file", "host_ring": "many"})
     assert st == 2 and "auto" in err
+
+
+@pytest.mark.parametrize("tier,R", [("host", 3), ("file", 2), ("host", "all")])
+def test_resident_groups_move_no_state_bytes(tier, R):
+    """resident_groups: optimizer groups g0..g(R-1) keep master/m/v in HBM —
+    their state hops (and, file tier, state file IO) move 0 B, the GPU pool
+    books their 12N B from the start, and the unchanged invariants still
+    hold on the mapped graph's DES."""
+    sc = C1_SSD if tier == "file" else C1
+    st, base, _, err = execute(sc, {"dry_run": True, "tier": tier})
+    assert st == 0, err
+    st, s, _, err = execute(sc, {"dry_run": True, "tier": tier, "resident_groups": R})
+    assert st == 0, err
+    assert s["all_invariants_pass"], s["invariants"]
+    r = L1 if R == "all" else R
+    mb, b0 = s["mapped_bytes"], base["mapped_bytes"]
+    assert mb.get("link_c2g/opt_states", 0) == b0["link_c2g/opt_states"] - 12 * N1 * r
+    assert mb.get("link_g2c/opt_states", 0) == b0["link_g2c/opt_states"] - 12 * N1 * r
+    assert mb["link_g2c/params"] == b0["link_g2c/params"]     # params still go to host
+    if tier == "file":
+        assert mb["link_ssd/opt_states"] == b0["link_ssd/opt_states"] - 24 * N1 * r
+
+
+def test_resident_groups_rejects_bad_value():
+    st, _, _, err = execute(C1, {"dry_run": True, "resident_groups": "some"})
+    assert st == 2 and "resident_groups" in err
