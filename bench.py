@@ -994,7 +994,8 @@ def iteration_phase(F):
     # a 4-block slice of the 13B shape (3.77 GB of states per block) where
     # per-operation overheads no longer dominate the planned timeline
     for tag, layers, heads, hidden, batch in (("c1_b8", 12, 12, 768, 8), ("c1_b128", 12, 12, 768, 128),
-                                              ("13b_shape_4_blocks_b8", 4, 40, 5120, 8)):
+                                              ("13b_shape_4_blocks_b8", 4, 40, 5120, 8),
+                                              ("13b_shape_4_blocks_b8_resident", 4, 40, 5120, 8)):
         sc = json.dumps({"schema_version": 1, "model": {"name": tag, "num_layers": layers,
                          "num_heads": heads, "hidden_dim": hidden, "batch_size": batch, "seq_len": 1024},
                          "hardware": "a100-12ssd", "variant": "overlapped"})
@@ -1006,6 +1007,9 @@ def iteration_phase(F):
             # real bf16 GEMMs beside the optimizer; each wgrad writes its
             # block's gradients, which the fused optimizer then consumes
             opts = {"tier": "host", "compute_mode": "gemm_dataflow"}
+        if tag.endswith("_resident"):
+            # the slice's 15 GB of optimizer states stay in HBM (resident_groups)
+            opts = {"tier": "host", "compute_mode": "gemm_dataflow", "resident_groups": "all"}
         st = L.offsim_execute(h, json.dumps(opts).encode(), C.byref(summ), None)
         L.offsim_scenario_free(h)
         d = json.loads(C.cast(summ, C.c_char_p).value.decode())
