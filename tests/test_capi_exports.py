@@ -138,3 +138,43 @@ def test_graph_execute_rejects_bad_input_without_gpu():
     assert b"12*h^2" in LIB.offsim_last_error()
     assert LIB.fy_graph_execute(sc, b'{"tier": "disk"}', None, 0, C.byref(out)) == 2
     assert not out.value
+
+
+def test_c_consumer_compiles_links_and_runs(tmp_path):
+    """A plain C11 program (no C++, no CUDA headers) includes both public C
+    headers, links liboffsim.so.0 and calls into it — what a cgo / JNI /
+    N-API / ctypes binding does."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2403_06504_b200" / "lib"
+    src = tmp_path / "consumer.c"
+    src.write_text(r'''
+#include "fuyou/fy_adam.h"
+#include "offsim/offsim_c.h"
+#include <stdio.h>
+#include <string.h>
+int main(void) {
+    char* report = NULL;
+    offsim_scenario* s = NULL;
+    if (offsim_scenario_from_preset("13b-a100-b32", &s) != OFFSIM_OK) return 2;
+    if (offsim_plan(s, &report) != OFFSIM_OK || !report || !strstr(report, "swap_coefficient")) return 3;
+    offsim_string_free(report);
+    offsim_scenario_free(s);
+    uint64_t off = 0, cnt = 0;
+    if (fy_shard_range(1000, 3, 1, 8, &off, &cnt) != FY_OK || off == 0 || cnt == 0) return 4;
+    if (fy_adamw_chunk(NULL, NULL) != FY_ERR_CONFIG || fy_last_error() == NULL) return 5;
+    printf("%s %s\n", offsim_version(), fy_version());
+    return 0;
+}
+''')
+    exe = tmp_path / "consumer"
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", f"-I{root / 'include'}", str(src),
+                        f"-L{lib}", "-l:liboffsim.so.0", f"-Wl,-rpath,{lib}", "-o", str(exe)],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
