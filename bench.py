@@ -993,7 +993,8 @@ def iteration_phase(F):
     # C1 (GPT-2-small shape) at b=8 and b=128 (13 swapped activations), and
     # a 4-block slice of the 13B shape (3.77 GB of states per block) where
     # per-operation overheads no longer dominate the planned timeline
-    for tag, layers, heads, hidden, batch in (("c1_b8", 12, 12, 768, 8), ("c1_b128", 12, 12, 768, 128),
+    for tag, layers, heads, hidden, batch in (("c1_b8", 12, 12, 768, 8), ("c1_b8_resident", 12, 12, 768, 8),
+                                              ("c1_b128", 12, 12, 768, 128),
                                               ("13b_shape_4_blocks_b8", 4, 40, 5120, 8),
                                               ("13b_shape_4_blocks_b8_resident", 4, 40, 5120, 8)):
         sc = json.dumps({"schema_version": 1, "model": {"name": tag, "num_layers": layers,
@@ -1008,8 +1009,9 @@ def iteration_phase(F):
             # block's gradients, which the fused optimizer then consumes
             opts = {"tier": "host", "compute_mode": "gemm_dataflow"}
         if tag.endswith("_resident"):
-            # the slice's 15 GB of optimizer states stay in HBM (resident_groups)
-            opts = {"tier": "host", "compute_mode": "gemm_dataflow", "resident_groups": "all"}
+            # all optimizer states stay in HBM (resident_groups): 1.0 GB for C1,
+            # 15.1 GB for the 13B slice
+            opts = {**opts, "resident_groups": "all"}
         st = L.offsim_execute(h, json.dumps(opts).encode(), C.byref(summ), None)
         L.offsim_scenario_free(h)
         d = json.loads(C.cast(summ, C.c_char_p).value.decode())
