@@ -94,9 +94,12 @@ struct ExecOptions {
     // Report an FNV-1a checksum of every chunk's final [master|m|v].
     bool checksum_states = false;
     // Optimizer groups g0..g(R-1) whose states stay resident in HBM (see
-    // map_graph_for_b200); 0xffffffff = all groups ("all").
+    // map_graph_for_b200); 0xffffffff = all groups ("all"); kResidentAuto =
+    // as many as the HBM left after the executor's own buffers holds ("auto").
     std::uint32_t resident_groups = 0;
 };
+
+inline constexpr std::uint32_t kResidentAuto = 0xfffffffeu;
 
 // Caller-provided optimizer states for chunk (block) k: pinned host
 // [master | m | v] (12n B) and the bf16 param output (2n B). When absent the
@@ -203,6 +206,7 @@ struct ExecReport {
     std::uint64_t pinned_host_bytes = 0;  // host staging the run allocated
     RingDepths host_ring;                 // staging ring depths (file tier)
     std::uint64_t state_checksum = 0;     // checksum_states
+    std::uint32_t resident_groups = 0;    // optimizer groups kept in HBM
 };
 
 ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const SwapPlan& plan,

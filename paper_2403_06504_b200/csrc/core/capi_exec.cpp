@@ -71,9 +71,10 @@ ParsedOptions parse_options(const char* text) {
         }
         o.checksum_states = doc.value("checksum_states", o.checksum_states);
         if (doc.contains("resident_groups") && doc.at("resident_groups").is_string()) {
-            if (doc.at("resident_groups").get<std::string>() != "all")
-                throw ConfigError("exec options: resident_groups must be a count or 'all'");
-            o.resident_groups = 0xffffffffu;
+            const std::string v = doc.at("resident_groups").get<std::string>();
+            if (v != "all" && v != "auto")
+                throw ConfigError("exec options: resident_groups must be a count, 'all' or 'auto'");
+            o.resident_groups = v == "all" ? 0xffffffffu : kResidentAuto;
         } else {
             o.resident_groups = doc.value("resident_groups", o.resident_groups);
         }
@@ -187,6 +188,7 @@ std::string exec_summary_json(const ExecReport& r) {
         {"pinned_host_bytes", r.pinned_host_bytes},
         {"host_ring", rings_json(r.host_ring)},
         {"state_checksum", r.state_checksum},
+        {"resident_groups", r.resident_groups},
         {"invariants", checks},
         {"all_invariants_pass", r.invariants.all_pass && r.swap_mismatches == 0},
     };
@@ -212,7 +214,8 @@ SwapPlan plan_with_placement(const Scenario& s, const std::string& placement) {
 std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVariant v) {
     const SwapPlan plan = plan_with_placement(s, po.placement);
     const TaskGraph ref = build_schedule(s.model, s.hardware, plan, v);
-    TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots, po.exec.resident_groups);
+    TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots,
+                                          po.exec.resident_groups == kResidentAuto ? 0 : po.exec.resident_groups);
     if (po.exec.swap_only) mapped = swap_subgraph(mapped, po.exec.max_blocks);
     const RingDepths rings = host_ring_depths(mapped, po.exec);
     add_host_ring_edges(mapped, rings);

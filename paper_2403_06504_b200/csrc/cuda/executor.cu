@@ -317,6 +317,11 @@ private:
     std::vector<Device> res_states_;  // resident optimizer groups g0..g(R-1): states in HBM
     std::uint32_t resident_ = 0;
     bool is_resident(std::uint32_t k) const { return k < resident_; }
+
+public:
+    std::uint32_t resident_count() const { return resident_; }
+
+private:
     void* read_tier_states(std::uint32_t k, Pinned& tmp);  // initial states of chunk k
     void write_back_resident();                             // after the run
     std::vector<const void*> d_grads_;
@@ -601,6 +606,16 @@ void Engine::setup() {
     }
     if (has_update_ && opt_.resident_groups > 0) {
         resident_ = std::min<std::uint32_t>(opt_.resident_groups, blocks_);
+        if (opt_.resident_groups == kResidentAuto) {
+            // every other buffer of the run is allocated by now; keep room for
+            // the calibration's scratch (14 B/param of one group) and a margin
+            std::size_t free_b = 0, total_b = 0;
+            check_cuda(cudaMemGetInfo(&free_b, &total_b), "meminfo");
+            const std::uint64_t keep = 14 * n_ + (1ull << 30) + total_b / 50;
+            resident_ = free_b > keep ? static_cast<std::uint32_t>(std::min<std::uint64_t>(
+                                            blocks_, (free_b - keep) / state_b))
+                                      : 0;
+        }
         Pinned tmp;
         for (std::uint32_t k = 0; k < resident_; ++k) {
             res_states_.emplace_back(state_b);
@@ -1141,6 +1156,15 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
 
     Engine eng(model, plan, rep.graph, options, chunks);
     eng.setup();
+    rep.resident_groups = eng.resident_count();
+    if (options.resident_groups == kResidentAuto && !options.swap_only) {
+        // the engine sized the resident groups from the HBM left free: map
+        // again with that count (same tasks and ids; state hops of resident
+        // groups now move 0 B and their states are booked up front)
+        rep.graph = map_graph_for_b200(reference, options.tier, std::max<std::uint32_t>(2, options.state_slots),
+                                       rep.resident_groups);
+        add_host_ring_edges(rep.graph, rep.host_ring);
+    }
     if (options.tier == StateTier::file) rep.io_engine = eng.io_engine();
     MeasuredRates rates = eng.calibrate();
     if (rates.compute_flops <= 0) rates.compute_flops = hw.gpu_tput;
