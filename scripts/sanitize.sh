@@ -28,4 +28,12 @@ NEW="multi_chunk_launch_bit_exact or batches_over_96 or device_side_clipping or 
    python -m pytest tests/test_adamw_gpu.py -q -x -k "multi_chunk_launch_bit_exact and tma or sweep_variants and 22541" > $OUT/${TAG}_synccheck_new_kernels.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_synccheck_new_kernels.log)
 (timeout 900 $CS --tool memcheck --error-exitcode 9 \
    python -m pytest tests/test_swap_gpu.py -q -x > $OUT/${TAG}_memcheck_swap.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_swap.log)
+# fp32 gradients on the TMA path (18 B/element stages)
+FP32="tma_bulk_path_bit_exact and 14341 and 2- or multi_chunk_launch_bit_exact and tma and 2-"
+(timeout 900 $CS --tool memcheck --error-exitcode 9 \
+   python -m pytest tests/test_adamw_gpu.py -q -x -k "$FP32" > $OUT/${TAG}_memcheck_fp32.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_fp32.log)
+(timeout 900 $CS --tool racecheck --error-exitcode 9 \
+   python -m pytest tests/test_adamw_gpu.py -q -x -k "$FP32" > $OUT/${TAG}_racecheck_fp32.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_racecheck_fp32.log)
+(timeout 900 $CS --tool synccheck --error-exitcode 9 \
+   python -m pytest tests/test_adamw_gpu.py -q -x -k "$FP32" > $OUT/${TAG}_synccheck_fp32.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_synccheck_fp32.log)
 tail -n 3 $OUT/${TAG}_*check*.log
