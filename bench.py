@@ -1146,7 +1146,7 @@ def swap_sweep_phase(F, budget_cpu=8e9, budget_ssd=2e9):
     return rows
 
 
-def ssd_tier_phase(F, blocks=8, ring=3):
+def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True):
     """Opt-in (--ssd-tier): one iteration of a 13B-shaped slice whose
     optimizer states live in FILES (O_DIRECT io_uring) and stream through a
     `ring`-slot pinned staging ring — the paper's SSD tier with host memory
@@ -1164,7 +1164,8 @@ def ssd_tier_phase(F, blocks=8, ring=3):
     h = P()
     assert L.offsim_scenario_parse(sc.encode(), C.byref(h)) == 0
     summ = P()
-    opts = {"tier": "file", "host_ring": ring, "compute_mode": "gemm", "file_dir": "/tmp/offsim_ssd_tier"}
+    opts = {"tier": "file", "host_ring": ring, "compute_mode": "gemm", "file_dir": "/tmp/offsim_ssd_tier",
+            "fixed_buffers": fixed_buffers}
     st = L.offsim_execute(h, json.dumps(opts).encode(), C.byref(summ), None)
     L.offsim_scenario_free(h)
     d = json.loads(C.cast(summ, C.c_char_p).value.decode())
@@ -1180,7 +1181,8 @@ def ssd_tier_phase(F, blocks=8, ring=3):
             "predicted_s": d["predicted"]["makespan_s"],
             "executed_over_predicted": d["executed_over_predicted"],
             "hw_predicted": d["hw_predicted"],
-            "io_engine": d["io_engine"], "all_invariants_pass": d["all_invariants_pass"],
+            "io_engine": d["io_engine"], "io_requests": d["io_requests"],
+            "all_invariants_pass": d["all_invariants_pass"],
             "optimizer_kernel_params_per_s": d["optimizer"]["kernel_params_per_s"]}
 
 

@@ -63,6 +63,7 @@ struct ExecOptions {
     StateTier tier = StateTier::host;
     std::string file_dir = "/tmp/offsim_b200";
     bool direct_io = true;          // O_DIRECT for the file tier
+    bool fixed_buffers = true;      // register the staging rings with io_uring (READ/WRITE_FIXED)
     double compute_rate = 0.0;      // FLOP/s of synthetic compute (0: hw.gpu_tput)
     // fwd/bwd compute tasks: "spin" = timed kernel of work / compute_rate
     // (no SM/HBM contention); "gemm" = the layer's real bf16 GEMMs through
@@ -203,6 +204,9 @@ struct ExecReport {
     std::uint64_t swap_mismatches = 0; // must be 0
     std::uint32_t kernel_launches = 0;
     std::string io_engine; // "io_uring" | "pread/pwrite" (file tier)
+    std::uint64_t io_registered_bytes = 0; // staging rings registered with io_uring
+    std::uint64_t io_fixed_requests = 0;   // file requests issued as READ/WRITE_FIXED
+    std::uint64_t io_plain_requests = 0;   // ... and as plain READ/WRITE
     std::uint64_t pinned_host_bytes = 0;  // host staging the run allocated
     RingDepths host_ring;                 // staging ring depths (file tier)
     std::uint64_t state_checksum = 0;     // checksum_states

@@ -43,7 +43,7 @@ ParsedOptions parse_options(const char* text) {
                                                "verify_swaps", "adam", "dry_run", "variant",
                                                "swap_only", "max_blocks", "placement",
                                                "compute_mode", "host_ring", "checksum_states",
-                                               "resident_groups"};
+                                               "resident_groups", "fixed_buffers"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -55,6 +55,7 @@ ParsedOptions parse_options(const char* text) {
         else throw ConfigError("exec options: tier must be 'host' or 'file'");
         o.file_dir = doc.value("file_dir", o.file_dir);
         o.direct_io = doc.value("direct_io", o.direct_io);
+        o.fixed_buffers = doc.value("fixed_buffers", o.fixed_buffers);
         o.compute_rate = doc.value("compute_rate", o.compute_rate);
         o.state_slots = doc.value("state_slots", o.state_slots);
         o.seed = doc.value("seed", o.seed);
@@ -185,6 +186,9 @@ std::string exec_summary_json(const ExecReport& r) {
         {"swap_mismatches", r.swap_mismatches},
         {"kernel_launches", r.kernel_launches},
         {"io_engine", r.io_engine},
+        {"io_requests", {{"registered_bytes", r.io_registered_bytes},
+                         {"fixed", r.io_fixed_requests},
+                         {"plain", r.io_plain_requests}}},
         {"pinned_host_bytes", r.pinned_host_bytes},
         {"host_ring", rings_json(r.host_ring)},
         {"state_checksum", r.state_checksum},

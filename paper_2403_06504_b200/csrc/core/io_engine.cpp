@@ -3,9 +3,11 @@
 
 #include <linux/io_uring.h>
 #include <sys/mman.h>
+#include <sys/uio.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cerrno>
 #include <cstring>
@@ -20,6 +22,9 @@ int uring_setup(unsigned entries, io_uring_params* p) {
 }
 int uring_enter(int fd, unsigned submit, unsigned wait, unsigned flags) {
     return static_cast<int>(::syscall(__NR_io_uring_enter, fd, submit, wait, flags, nullptr, 0));
+}
+int uring_register(int fd, unsigned op, const void* arg, unsigned n) {
+    return static_cast<int>(::syscall(__NR_io_uring_register, fd, op, arg, n));
 }
 template <typename T>
 T* at(void* base, std::uint32_t off) {
@@ -67,10 +72,48 @@ IoEngine::IoEngine(unsigned depth, std::uint64_t piece) : depth_(depth), piece_(
 }
 
 IoEngine::~IoEngine() {
+    unregister_buffers();
     if (sqes_ && sqes_ != MAP_FAILED) ::munmap(sqes_, sqes_len_);
     if (cq_ptr_ && cq_ptr_ != MAP_FAILED && cq_ptr_ != sq_ptr_) ::munmap(cq_ptr_, cq_len_);
     if (sq_ptr_ && sq_ptr_ != MAP_FAILED) ::munmap(sq_ptr_, sq_len_);
     if (ring_fd_ >= 0) ::close(ring_fd_);
+}
+
+std::uint64_t IoEngine::register_buffers(const std::vector<std::pair<void*, std::uint64_t>>& bufs) {
+    unregister_buffers();
+    if (ring_fd_ < 0) return 0;
+    constexpr std::uint64_t kMaxPiece = 1ull << 30;
+    std::vector<iovec> iov;
+    std::vector<Region> regions;
+    for (const auto& [p, bytes] : bufs) {
+        for (std::uint64_t off = 0; off < bytes; off += kMaxPiece) {
+            const std::uint64_t len = std::min(kMaxPiece, bytes - off);
+            iov.push_back(iovec{static_cast<char*>(p) + off, static_cast<std::size_t>(len)});
+            regions.push_back(Region{reinterpret_cast<std::uint64_t>(p) + off, len,
+                                     static_cast<unsigned>(iov.size() - 1)});
+        }
+    }
+    if (iov.empty()) return 0;
+    if (uring_register(ring_fd_, IORING_REGISTER_BUFFERS, iov.data(), static_cast<unsigned>(iov.size())) < 0)
+        return 0;
+    std::sort(regions.begin(), regions.end(), [](const Region& a, const Region& b) { return a.base < b.base; });
+    regions_ = std::move(regions);
+    std::uint64_t total = 0;
+    for (const Region& r : regions_) total += r.len;
+    return total;
+}
+
+void IoEngine::unregister_buffers() {
+    if (ring_fd_ >= 0 && !regions_.empty()) uring_register(ring_fd_, IORING_UNREGISTER_BUFFERS, nullptr, 0);
+    regions_.clear();
+}
+
+int IoEngine::fixed_index(std::uint64_t p, std::uint64_t len) const {
+    auto it = std::upper_bound(regions_.begin(), regions_.end(), p,
+                               [](std::uint64_t x, const Region& r) { return x < r.base; });
+    if (it == regions_.begin()) return -1;
+    --it;
+    return p + len <= it->base + it->len ? static_cast<int>(it->index) : -1;
 }
 
 std::string IoEngine::transfer_sync(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset,
@@ -106,10 +149,18 @@ std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint
             const unsigned idx = tail & *sq_mask_;
             io_uring_sqe& e = sqes[idx];
             std::memset(&e, 0, sizeof e);
-            e.opcode = write ? IORING_OP_WRITE : IORING_OP_READ;
             e.fd = fd;
             e.addr = reinterpret_cast<std::uint64_t>(static_cast<char*>(buf) + off);
             e.len = static_cast<std::uint32_t>(std::min(piece_, bytes - off));
+            const int fixed = regions_.empty() ? -1 : fixed_index(e.addr, e.len);
+            if (fixed >= 0) {
+                e.opcode = write ? IORING_OP_WRITE_FIXED : IORING_OP_READ_FIXED;
+                e.buf_index = static_cast<std::uint16_t>(fixed);
+                ++fixed_requests_;
+            } else {
+                e.opcode = write ? IORING_OP_WRITE : IORING_OP_READ;
+                ++plain_requests_;
+            }
             e.off = offset + off;
             e.user_data = next;
             sq_array_[idx] = idx;

@@ -4,10 +4,16 @@
 // bandwidth (the reference's SSD lane is n_ssd devices, hardware.cpp:39-42).
 // Falls back to a pread/pwrite loop when io_uring_setup is refused (old
 // kernel or a sandbox seccomp policy); `engine()` reports which one ran.
+// Long-lived staging buffers (the executor's pinned rings, the swap
+// engine's slots) can be registered with the ring once: requests that fall
+// inside them go out as READ_FIXED / WRITE_FIXED, so the kernel does not
+// pin and unpin the pages of every request.
 #pragma once
 
 #include <cstdint>
 #include <string>
+#include <utility>
+#include <vector>
 
 namespace fy {
 
@@ -24,6 +30,16 @@ public:
     std::string transfer(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset, bool write);
 
     const char* engine() const { return ring_fd_ >= 0 ? "io_uring" : "pread/pwrite"; }
+
+    // Registers (base, bytes) buffers, replacing any earlier registration;
+    // each is split into <= 1 GiB pieces (the kernel's per-buffer limit).
+    // Returns the registered bytes (0 on the fallback engine or when the
+    // kernel refuses, e.g. RLIMIT_MEMLOCK; transfers then use plain ops).
+    std::uint64_t register_buffers(const std::vector<std::pair<void*, std::uint64_t>>& bufs);
+    void unregister_buffers();
+    // requests issued so far as fixed-buffer / plain io_uring ops
+    std::uint64_t fixed_requests() const { return fixed_requests_; }
+    std::uint64_t plain_requests() const { return plain_requests_; }
 
 private:
     std::string transfer_sync(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset, bool write);
@@ -44,6 +60,14 @@ private:
     unsigned* cq_tail_ = nullptr;
     unsigned* cq_mask_ = nullptr;
     void* cqes_ = nullptr;
+    struct Region {
+        std::uint64_t base, len;
+        unsigned index;
+    };
+    std::vector<Region> regions_; // sorted by base
+    std::uint64_t fixed_requests_ = 0, plain_requests_ = 0;
+    // index of the registered buffer holding [p, p + len), or -1
+    int fixed_index(std::uint64_t p, std::uint64_t len) const;
 };
 
 } // namespace fy

@@ -257,6 +257,9 @@ public:
     void setup();
     MeasuredRates calibrate();
     const char* io_engine() const { return io_.engine(); }
+    std::uint64_t io_registered() const { return io_registered_; }
+    std::uint64_t io_fixed() const { return io_.fixed_requests(); }
+    std::uint64_t io_plain() const { return io_.plain_requests(); }
     void run(const SimTrace& planned, ExecReport& rep);
 
 private:
@@ -283,6 +286,9 @@ private:
     RingDepths depths_;
     bool acts_on_ssd_ = false;
     std::vector<Pinned> state_ring_, param_ring_, weight_ring_, act_ring_;
+    // staging buffers registered with io_uring (READ/WRITE_FIXED requests)
+    std::vector<std::pair<void*, std::uint64_t>> io_bufs_;
+    std::uint64_t io_registered_ = 0;
     std::map<std::uint32_t, int> ring_slot_; // task id -> ring slot
     std::uint64_t pinned_bytes_ = 0;
     Pinned pin(std::uint64_t bytes) {
@@ -492,6 +498,18 @@ void Engine::setup() {
         for (std::uint32_t r = 0; r < depths_.weights; ++r) weight_ring_.push_back(pin(round_up(max_w)));
         for (std::uint32_t r = 0; r < depths_.acts; ++r) act_ring_.push_back(pin(round_up(max_act)));
         assign_ring_slots();
+        if (opt_.fixed_buffers) {
+            // the rings are every file request's host side: register them
+            // once so the kernel does not pin / unpin pages per request
+            const auto add = [&](const std::vector<Pinned>& r, std::uint64_t b) {
+                for (const Pinned& x : r) io_bufs_.emplace_back(x.p, std::max<std::uint64_t>(b, kAlign));
+            };
+            add(state_ring_, round_up(state_b));
+            add(param_ring_, round_up(param_b));
+            add(weight_ring_, round_up(max_w));
+            add(act_ring_, round_up(max_act));
+            io_registered_ = io_.register_buffers(io_bufs_);
+        }
     }
 
     dataflow_ = opt_.compute_mode == "gemm_dataflow";
@@ -738,6 +756,21 @@ MeasuredRates Engine::calibrate() {
         const bool direct = opt_.direct_io && model_.hidden_dim % 64 == 0;
         TierFile probe_file(opt_.file_dir + "/offsim_" + std::to_string(::getpid()) + "_probe.bin",
                             round_up(bytes), direct);
+        // the probe buffer joins the registration while it is in use, so the
+        // calibrated rates are those of the requests the iteration issues
+        if (io_registered_) {
+            auto with_probe = io_bufs_;
+            with_probe.emplace_back(h.p, round_up(bytes));
+            io_registered_ = io_.register_buffers(with_probe) ? io_registered_ : 0;
+        }
+        // back to the rings alone before the probe buffer is freed (a stale
+        // registration would alias whatever is mapped there next)
+        struct Reregister {
+            Engine* e;
+            ~Reregister() {
+                if (e->io_registered_) e->io_registered_ = e->io_.register_buffers(e->io_bufs_);
+            }
+        } reregister{this};
         IoRequest w{&io_, probe_file.fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
                     &io_error_text_, &io_mu_};
         IoRequest rd = w;
@@ -1167,12 +1200,16 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
     }
     if (options.tier == StateTier::file) rep.io_engine = eng.io_engine();
     MeasuredRates rates = eng.calibrate();
+    rep.io_registered_bytes = eng.io_registered();
+    const std::uint64_t cal_fixed = eng.io_fixed(), cal_plain = eng.io_plain();
     if (rates.compute_flops <= 0) rates.compute_flops = hw.gpu_tput;
     rep.hw_exec = b200_hardware(hw, rates);
     rep.planned = simulate(rep.graph, rep.hw_exec);
     rep.hw_predicted = b200_hardware_effective(hw, rates);
     rep.predicted = simulate(rep.graph, rep.hw_predicted);
     eng.run(rep.planned, rep);
+    rep.io_fixed_requests = eng.io_fixed() - cal_fixed;  // the iteration's requests only
+    rep.io_plain_requests = eng.io_plain() - cal_plain;
     rep.invariants = check_trace_invariants(rep.graph, rep.trace, rep.hw_exec);
     return rep;
 }

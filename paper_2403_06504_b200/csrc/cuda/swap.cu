@@ -76,6 +76,7 @@ void Swapper::release_all() noexcept {
     for (auto& [cap, p] : free_host_)
         if (!host_free(p)) cudaFreeHost(p);
     free_host_.clear();
+    io_.unregister_buffers();
     for (void* p : slots_)
         if (!host_free(p)) cudaFreeHost(p);
     slots_.clear();
@@ -117,6 +118,11 @@ void Swapper::open_file() {
             check_cuda(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
             slot_filled_.push_back(b);
         }
+        // every file request's host side is a slot: register the ring with
+        // io_uring once (READ/WRITE_FIXED; plain ops if the kernel refuses)
+        std::vector<std::pair<void*, std::uint64_t>> bufs;
+        for (void* p : slots_) bufs.emplace_back(p, cfg_.slot_bytes);
+        io_.register_buffers(bufs);
     } catch (...) {
         for (void* p : slots_)
             if (!host_free(p)) cudaFreeHost(p);

@@ -57,6 +57,11 @@ int main(int argc, char** argv) {
     if (fd < 0) fd = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
     if (fd < 0) return 4;
     fy::IoEngine io(depth, 1ull << 20);
+    // "fixed": register both buffers (b in two halves) -> READ/WRITE_FIXED
+    const bool fixed = argc > 4 && std::string(argv[4]) == "fixed";
+    std::uint64_t reg = 0;
+    if (fixed)
+        reg = io.register_buffers({{a, bytes}, {b, bytes / 2}, {static_cast<char*>(b) + bytes / 2, bytes - bytes / 2}});
     const auto t0 = std::chrono::steady_clock::now();
     std::string err = io.transfer(fd, a, bytes, 0, true);
     const auto t1 = std::chrono::steady_clock::now();
@@ -71,6 +76,8 @@ int main(int argc, char** argv) {
     const bool same = std::memcmp(a, b, bytes) == 0;
     const double w = bytes / 1e6 / std::chrono::duration<double>(t1 - t0).count();
     const double r = bytes / 1e6 / std::chrono::duration<double>(t2 - t1).count();
-    std::printf("%s %s %.0f %.0f\n", io.engine(), same ? "OK" : "MISMATCH", w, r);
+    std::printf("%s %s %.0f %.0f fixed=%llu plain=%llu registered=%llu\n", io.engine(), same ? "OK" : "MISMATCH", w,
+                r, static_cast<unsigned long long>(io.fixed_requests()),
+                static_cast<unsigned long long>(io.plain_requests()), static_cast<unsigned long long>(reg));
     return same ? 0 : 1;
 }

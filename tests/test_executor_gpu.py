@@ -177,6 +177,17 @@ def test_file_tier_bounded_ring_matches_host_tier(cuda_dev, tmp_path):
             assert ring["pinned_host_bytes"] < host["pinned_host_bytes"] / 2
         else:  # depths from the reference schedule's windows
             assert ring["host_ring"]["states"] == 3 and ring["host_ring"]["weights"] >= 2
+        io = ring["io_requests"]
+        if ring["io_engine"] == "io_uring" and io["registered_bytes"] > 0:
+            # every file request's host side is a registered ring slot
+            assert io["fixed"] > 0 and io["plain"] == 0, io
+    # registration off: the same result through plain requests
+    st, plain, _, err = execute(sc, {"tier": "file", "file_dir": str(tmp_path), "host_ring": 2,
+                                     "compute_rate": RATE, "checksum_states": True, "seed": 5,
+                                     "fixed_buffers": False})
+    assert st == 0, (err, _failing(plain))
+    assert plain["state_checksum"] == host["state_checksum"]
+    assert plain["io_requests"]["fixed"] == 0 and plain["io_requests"]["registered_bytes"] == 0
 
 
 def test_gemm_dataflow_grads_feed_the_optimizer(cuda_dev):

@@ -33,3 +33,24 @@ def test_io_engine_reports_injected_faults(tmp_path, depth):
                        timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAULTS-REPORTED" in r.stdout
+
+
+@pytest.mark.parametrize("mib,depth", [(8, 32), (3, 1), (17, 4)])
+def test_io_engine_registered_buffers(tmp_path, mib, depth):
+    """Registered (fixed) buffers: requests inside a registered buffer go out
+    as READ_FIXED / WRITE_FIXED, a request straddling two registrations as a
+    plain op (odd sizes split the read buffer mid-request), data bit-exact."""
+    if not EXE.exists():
+        pytest.skip("build/io_engine_test not built")
+    r = subprocess.run([str(EXE), str(tmp_path), str(mib), str(depth), "fixed"], capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    f = r.stdout.split()
+    assert f[1] == "OK"
+    kv = dict(x.split("=") for x in f[4:])
+    if f[0] != "io_uring" or int(kv["registered"]) == 0:
+        pytest.skip(f"registration unavailable here ({f[0]}, registered={kv['registered']})")
+    assert int(kv["registered"]) == 2 * (mib << 20)
+    straddle = mib % 2  # the read buffer's halves meet mid-request for odd MiB
+    assert int(kv["plain"]) == straddle
+    assert int(kv["fixed"]) == 2 * mib - straddle
