@@ -1127,6 +1127,10 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
     check_cuda(cudaMemcpy(&rep.grad_sq_sum, d_norm_.p, sizeof(double), cudaMemcpyDeviceToHost), "norm");
     rep.expected_grad_sq_sum = dataflow_ ? expected_grad_sq_ : -1.0;
     rep.pinned_host_bytes = pinned_bytes_;
+    // the iteration's file requests (the write-back / checksum reads below
+    // use scratch buffers outside the registration)
+    rep.io_fixed_requests = io_.fixed_requests();
+    rep.io_plain_requests = io_.plain_requests();
     if (resident_ > 0) write_back_resident();
     if (opt_.checksum_states && has_update_) rep.state_checksum = checksum_states();
     check_cuda(cudaMemcpy(&rep.nonfinite, d_bad_.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
@@ -1208,8 +1212,8 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
     rep.hw_predicted = b200_hardware_effective(hw, rates);
     rep.predicted = simulate(rep.graph, rep.hw_predicted);
     eng.run(rep.planned, rep);
-    rep.io_fixed_requests = eng.io_fixed() - cal_fixed;  // the iteration's requests only
-    rep.io_plain_requests = eng.io_plain() - cal_plain;
+    rep.io_fixed_requests -= cal_fixed;  // the iteration's requests only
+    rep.io_plain_requests -= cal_plain;
     rep.invariants = check_trace_invariants(rep.graph, rep.trace, rep.hw_exec);
     return rep;
 }
