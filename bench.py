@@ -213,11 +213,21 @@ def barrier(world):
 
 # ------------------------------------------------------------ CPU baseline
 
+def host_threads() -> int:
+    """Every host thread this process may run on. Not omp_get_max_threads():
+    torchrun exports OMP_NUM_THREADS=1 to each rank, which would time the CPU
+    arm single-threaded under --gpus N > 1."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def cpu_oracle_rate(chunk: int, nchunks: int, target_s: float = 12.0, max_reps: int = 200):
     """Oracle port (DeepSpeed CPU Adam restatement) over all host threads on
     `nchunks` chunks of `chunk` params; returns (params/s, threads, sample)."""
     from oracle import oracle as O
-    threads = O.max_threads()
+    threads = host_threads()
     n = chunk * nchunks
     master = np.empty(n, np.float32)
     m = np.empty(n, np.float32)
@@ -1146,7 +1156,7 @@ def swap_sweep_phase(F, budget_cpu=8e9, budget_ssd=2e9):
     return rows
 
 
-def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True):
+def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True, file_dir="/tmp/offsim_ssd_tier"):
     """Opt-in (--ssd-tier): one iteration of a 13B-shaped slice whose
     optimizer states live in FILES (O_DIRECT io_uring) and stream through a
     `ring`-slot pinned staging ring — the paper's SSD tier with host memory
@@ -1164,7 +1174,7 @@ def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True):
     h = P()
     assert L.offsim_scenario_parse(sc.encode(), C.byref(h)) == 0
     summ = P()
-    opts = {"tier": "file", "host_ring": ring, "compute_mode": "gemm", "file_dir": "/tmp/offsim_ssd_tier",
+    opts = {"tier": "file", "host_ring": ring, "compute_mode": "gemm", "file_dir": file_dir,
             "fixed_buffers": fixed_buffers}
     st = L.offsim_execute(h, json.dumps(opts).encode(), C.byref(summ), None)
     L.offsim_scenario_free(h)
@@ -1181,7 +1191,7 @@ def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True):
             "predicted_s": d["predicted"]["makespan_s"],
             "executed_over_predicted": d["executed_over_predicted"],
             "hw_predicted": d["hw_predicted"],
-            "io_engine": d["io_engine"], "io_requests": d["io_requests"],
+            "io_engine": d["io_engine"], "io_requests": d["io_requests"], "file_devices": d["file_devices"],
             "all_invariants_pass": d["all_invariants_pass"],
             "optimizer_kernel_params_per_s": d["optimizer"]["kernel_params_per_s"]}
 
@@ -1242,7 +1252,7 @@ def run_reference(args):
     from oracle import oracle as O
     N = 12 * args.hidden * args.hidden
     nchunks = 4
-    threads = O.max_threads()
+    threads = host_threads()
     n = N * nchunks
     master = np.empty(n, np.float32)
     m = np.empty(n, np.float32)

@@ -62,6 +62,7 @@ struct ExecOptions {
     int device = 0;
     StateTier tier = StateTier::host;
     std::string file_dir = "/tmp/offsim_b200";
+    std::vector<std::string> file_dirs; // >1: tier files striped RAID-0 over these (one per SSD)
     bool direct_io = true;          // O_DIRECT for the file tier
     bool fixed_buffers = true;      // register the staging rings with io_uring (READ/WRITE_FIXED)
     double compute_rate = 0.0;      // FLOP/s of synthetic compute (0: hw.gpu_tput)
@@ -204,6 +205,7 @@ struct ExecReport {
     std::uint64_t swap_mismatches = 0; // must be 0
     std::uint32_t kernel_launches = 0;
     std::string io_engine; // "io_uring" | "pread/pwrite" (file tier)
+    std::uint32_t file_devices = 0;        // tier files striped over this many directories
     std::uint64_t io_registered_bytes = 0; // staging rings registered with io_uring
     std::uint64_t io_fixed_requests = 0;   // file requests issued as READ/WRITE_FIXED
     std::uint64_t io_plain_requests = 0;   // ... and as plain READ/WRITE

@@ -53,7 +53,17 @@ ParsedOptions parse_options(const char* text) {
         if (tier == "host") o.tier = StateTier::host;
         else if (tier == "file") o.tier = StateTier::file;
         else throw ConfigError("exec options: tier must be 'host' or 'file'");
-        o.file_dir = doc.value("file_dir", o.file_dir);
+        if (doc.contains("file_dir") && doc["file_dir"].is_array()) {
+            // one directory per SSD: the tier files are striped over them
+            for (const auto& d : doc["file_dir"]) o.file_dirs.push_back(d.get<std::string>());
+            if (o.file_dirs.empty()) throw ConfigError("exec options: file_dir list is empty");
+            if (o.file_dirs.size() > 64) throw ConfigError("exec options: at most 64 file_dir entries");
+            if (std::set<std::string>(o.file_dirs.begin(), o.file_dirs.end()).size() != o.file_dirs.size())
+                throw ConfigError("exec options: file_dir entries must be distinct");
+            o.file_dir = o.file_dirs.front();
+        } else {
+            o.file_dir = doc.value("file_dir", o.file_dir);
+        }
         o.direct_io = doc.value("direct_io", o.direct_io);
         o.fixed_buffers = doc.value("fixed_buffers", o.fixed_buffers);
         o.compute_rate = doc.value("compute_rate", o.compute_rate);
@@ -186,6 +196,7 @@ std::string exec_summary_json(const ExecReport& r) {
         {"swap_mismatches", r.swap_mismatches},
         {"kernel_launches", r.kernel_launches},
         {"io_engine", r.io_engine},
+        {"file_devices", r.file_devices},
         {"io_requests", {{"registered_bytes", r.io_registered_bytes},
                          {"fixed", r.io_fixed_requests},
                          {"plain", r.io_plain_requests}}},

@@ -134,8 +134,44 @@ std::string IoEngine::transfer_sync(int fd, void* buf, std::uint64_t bytes, std:
 
 std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset,
                                bool write) {
-    if (ring_fd_ < 0) return transfer_sync(fd, buf, bytes, offset, write);
-    const std::uint64_t pieces = (bytes + piece_ - 1) / piece_;
+    const Stripe one{&fd, 1, ~0ull};
+    return transfer(one, buf, bytes, offset, write);
+}
+
+std::string IoEngine::transfer(const Stripe& st, void* buf, std::uint64_t bytes, std::uint64_t offset,
+                               bool write) {
+    // split at stripe-unit boundaries (device changes) and at piece_ (the
+    // request size), then keep up to depth_ requests in flight
+    std::vector<Req> reqs;
+    char* p = static_cast<char*>(buf);
+    for (std::uint64_t o = offset, end = offset + bytes; o < end;) {
+        int fd = st.fds[0];
+        std::uint64_t dev_off = o, seg = end - o;
+        if (st.count > 1) {
+            const std::uint64_t s = o / st.unit, in = o % st.unit;
+            fd = st.fds[s % st.count];
+            dev_off = (s / st.count) * st.unit + in;
+            seg = std::min(seg, st.unit - in);
+        }
+        for (std::uint64_t done = 0; done < seg;) {
+            const std::uint64_t len = std::min(piece_, seg - done);
+            reqs.push_back(Req{fd, p + (o - offset) + done, len, dev_off + done});
+            done += len;
+        }
+        o += seg;
+    }
+    if (ring_fd_ < 0) {
+        for (const Req& r : reqs) {
+            const std::string err = transfer_sync(r.fd, r.buf, r.len, r.off, write);
+            if (!err.empty()) return err;
+        }
+        return {};
+    }
+    return submit(reqs, write);
+}
+
+std::string IoEngine::submit(const std::vector<Req>& reqs, bool write) {
+    const std::uint64_t pieces = reqs.size();
     auto* sqes = static_cast<io_uring_sqe*>(sqes_);
     auto* cqes = static_cast<io_uring_cqe*>(cqes_);
     std::vector<std::uint64_t> short_pieces;
@@ -145,13 +181,14 @@ std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint
         unsigned queued = 0;
         unsigned tail = __atomic_load_n(sq_tail_, __ATOMIC_RELAXED);
         while (next < pieces && inflight + unsubmitted + queued < depth_) {
-            const std::uint64_t off = next * piece_;
+            const Req& q = reqs[next];
             const unsigned idx = tail & *sq_mask_;
             io_uring_sqe& e = sqes[idx];
             std::memset(&e, 0, sizeof e);
-            e.fd = fd;
-            e.addr = reinterpret_cast<std::uint64_t>(static_cast<char*>(buf) + off);
-            e.len = static_cast<std::uint32_t>(std::min(piece_, bytes - off));
+            e.fd = q.fd;
+            e.addr = reinterpret_cast<std::uint64_t>(q.buf);
+            e.len = static_cast<std::uint32_t>(q.len);
+            e.off = q.off;
             const int fixed = regions_.empty() ? -1 : fixed_index(e.addr, e.len);
             if (fixed >= 0) {
                 e.opcode = write ? IORING_OP_WRITE_FIXED : IORING_OP_READ_FIXED;
@@ -161,7 +198,6 @@ std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint
                 e.opcode = write ? IORING_OP_WRITE : IORING_OP_READ;
                 ++plain_requests_;
             }
-            e.off = offset + off;
             e.user_data = next;
             sq_array_[idx] = idx;
             ++tail;
@@ -183,10 +219,9 @@ std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint
         const unsigned ctail = __atomic_load_n(cq_tail_, __ATOMIC_ACQUIRE);
         while (head != ctail) {
             const io_uring_cqe& c = cqes[head & *cq_mask_];
-            const std::uint64_t piece_idx = c.user_data;
-            const std::uint64_t want = std::min(piece_, bytes - piece_idx * piece_);
+            const std::uint64_t i = c.user_data;
             if (c.res < 0) failed_errno = static_cast<std::uint64_t>(-c.res);
-            else if (static_cast<std::uint64_t>(c.res) != want) short_pieces.push_back(piece_idx);
+            else if (static_cast<std::uint64_t>(c.res) != reqs[i].len) short_pieces.push_back(i);
             ++head;
             --inflight;
         }
@@ -196,9 +231,8 @@ std::string IoEngine::transfer(int fd, void* buf, std::uint64_t bytes, std::uint
         return std::string(write ? "io_uring write" : "io_uring read") + " failed: " +
                std::strerror(static_cast<int>(failed_errno));
     for (const std::uint64_t i : short_pieces) { // rare: finish synchronously
-        const std::uint64_t off = i * piece_;
-        const std::string err =
-            transfer_sync(fd, static_cast<char*>(buf) + off, std::min(piece_, bytes - off), offset + off, write);
+        const Req& q = reqs[i];
+        const std::string err = transfer_sync(q.fd, q.buf, q.len, q.off, write);
         if (!err.empty()) return err;
     }
     return {};

@@ -29,6 +29,18 @@ public:
     // success or an error message. Thread-compatible (one caller at a time).
     std::string transfer(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset, bool write);
 
+    // A logical file striped over `count` files (one per device): logical
+    // byte o lives in fds[(o / unit) % count] at ((o / unit) / count) * unit
+    // + o % unit — RAID-0 over the reference's n_ssd devices
+    // (hardware.cpp:39-42 aggregates their bandwidth). One ring drives all
+    // of them, so every device has requests in flight at once.
+    struct Stripe {
+        const int* fds;
+        unsigned count;
+        std::uint64_t unit; // multiple of 4 KiB
+    };
+    std::string transfer(const Stripe& st, void* buf, std::uint64_t bytes, std::uint64_t offset, bool write);
+
     const char* engine() const { return ring_fd_ >= 0 ? "io_uring" : "pread/pwrite"; }
 
     // Registers (base, bytes) buffers, replacing any earlier registration;
@@ -43,6 +55,12 @@ public:
 
 private:
     std::string transfer_sync(int fd, void* buf, std::uint64_t bytes, std::uint64_t offset, bool write);
+    struct Req {
+        int fd;
+        char* buf;
+        std::uint64_t len, off;
+    };
+    std::string submit(const std::vector<Req>& reqs, bool write);
 
     int ring_fd_ = -1;
     unsigned depth_ = 0;

@@ -105,7 +105,7 @@ __global__ void count_mismatch(const std::uint64_t* a, const std::uint64_t* b, s
 
 struct IoRequest {
     fy::IoEngine* io = nullptr;
-    int fd = -1;
+    fy::IoEngine::Stripe file{}; // the tier file's device files
     void* buf = nullptr;
     std::uint64_t bytes = 0; // rounded to kAlign for O_DIRECT
     std::uint64_t offset = 0;
@@ -128,7 +128,7 @@ void CUDART_CB run_io(void* arg) {
     auto* r = static_cast<IoRequest*>(arg);
     std::string err;
     try {  // nothing may escape a CUDA host callback
-        err = r->io->transfer(r->fd, r->buf, r->bytes, r->offset, r->write);
+        err = r->io->transfer(r->file, r->buf, r->bytes, r->offset, r->write);
     } catch (const std::exception& e) {
         err = std::string("file tier IO: ") + e.what();
     } catch (...) {
@@ -143,31 +143,55 @@ void CUDART_CB run_io(void* arg) {
     if (r->write && r->poison_after) std::memset(r->buf, 0xA5, r->bytes);
 }
 
+// One logical tier file, striped RAID-0 over one file per directory (one
+// directory per SSD: the reference's n_ssd devices, hardware.cpp:39-42) in
+// kStripeUnit pieces; a single directory is a plain file.
+constexpr std::uint64_t kStripeUnit = 4ull << 20;
+
 class TierFile {
 public:
-    TierFile(const std::string& path, std::uint64_t size, bool direct) : path_(path) {
-        int flags = O_RDWR | O_CREAT | O_TRUNC;
-        if (direct) flags |= O_DIRECT;
-        fd_ = ::open(path.c_str(), flags, 0600);
-        if (fd_ < 0 && direct) fd_ = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
-        if (fd_ < 0) throw InfeasibleError("cannot open tier file " + path + ": " + std::strerror(errno));
-        if (::ftruncate(fd_, static_cast<off_t>(size)) != 0) {
-            const std::string why = std::strerror(errno);
-            ::close(fd_);
-            ::unlink(path_.c_str());
-            fd_ = -1;
-            throw InfeasibleError("cannot size tier file " + path + ": " + why);
+    TierFile(const std::vector<std::string>& dirs, const std::string& name, std::uint64_t size, bool direct) {
+        const std::uint64_t count = dirs.size();
+        const std::uint64_t units = (size + kStripeUnit - 1) / kStripeUnit;
+        const std::uint64_t per_dev = count == 1 ? size : (units + count - 1) / count * kStripeUnit;
+        for (const std::string& dir : dirs) {
+            const std::string path = dir + "/" + name;
+            int flags = O_RDWR | O_CREAT | O_TRUNC;
+            if (direct) flags |= O_DIRECT;
+            int fd = ::open(path.c_str(), flags, 0600);
+            if (fd < 0 && direct) fd = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
+            if (fd < 0) {
+                const std::string why = std::strerror(errno);
+                close_all();
+                throw InfeasibleError("cannot open tier file " + path + ": " + why);
+            }
+            fds_.push_back(fd);
+            paths_.push_back(path);
+            if (::ftruncate(fd, static_cast<off_t>(per_dev)) != 0) {
+                const std::string why = std::strerror(errno);
+                close_all();
+                throw InfeasibleError("cannot size tier file " + path + ": " + why);
+            }
         }
     }
-    ~TierFile() {
-        if (fd_ >= 0) ::close(fd_);
-        ::unlink(path_.c_str());
+    ~TierFile() { close_all(); }
+    TierFile(const TierFile&) = delete;
+    TierFile& operator=(const TierFile&) = delete;
+    fy::IoEngine::Stripe stripe() const {
+        return {fds_.data(), static_cast<unsigned>(fds_.size()), kStripeUnit};
     }
-    int fd() const { return fd_; }
 
 private:
-    std::string path_;
-    int fd_ = -1;
+    void close_all() noexcept {
+        for (std::size_t i = 0; i < fds_.size(); ++i) {
+            ::close(fds_[i]);
+            ::unlink(paths_[i].c_str());
+        }
+        fds_.clear();
+        paths_.clear();
+    }
+    std::vector<int> fds_;
+    std::vector<std::string> paths_;
 };
 
 // ------------------------------------------------------------- parsing
@@ -258,6 +282,9 @@ public:
     MeasuredRates calibrate();
     const char* io_engine() const { return io_.engine(); }
     std::uint64_t io_registered() const { return io_registered_; }
+    std::vector<std::string> file_dirs() const {
+        return opt_.file_dirs.empty() ? std::vector<std::string>{opt_.file_dir} : opt_.file_dirs;
+    }
     std::uint64_t io_fixed() const { return io_.fixed_requests(); }
     std::uint64_t io_plain() const { return io_.plain_requests(); }
     void run(const SimTrace& planned, ExecReport& rep);
@@ -573,13 +600,13 @@ void Engine::setup() {
     check_cuda(cudaMemset(d_mismatch_.p, 0, sizeof(unsigned long long)), "memset");
 
     if (file_tier_) {
-        ::mkdir(opt_.file_dir.c_str(), 0700);
+        for (const std::string& d : file_dirs()) ::mkdir(d.c_str(), 0700);
         const bool direct = opt_.direct_io && model_.hidden_dim % 64 == 0;
-        const std::string stem = opt_.file_dir + "/offsim_" + std::to_string(::getpid()) + "_";
+        const std::string stem = "offsim_" + std::to_string(::getpid()) + "_";
         const bool chunks = has_update_ || has_weights_;
-        f_states_ = std::make_unique<TierFile>(stem + "states.bin",
+        f_states_ = std::make_unique<TierFile>(file_dirs(), stem + "states.bin",
                                                chunks ? blocks_ * round_up(state_b) : kAlign, direct);
-        f_params_ = std::make_unique<TierFile>(stem + "params.bin",
+        f_params_ = std::make_unique<TierFile>(file_dirs(), stem + "params.bin",
                                                chunks ? blocks_ * round_up(param_b) : kAlign, direct);
         std::uint64_t off = 0;
         act_file_off_.assign(layers_.size(), 0);
@@ -592,9 +619,9 @@ void Engine::setup() {
             ckpt_file_off_.push_back(off);
             off += round_up(ckpt_bytes_);
         }
-        f_acts_ = std::make_unique<TierFile>(stem + "acts.bin", std::max<std::uint64_t>(off, kAlign), direct);
+        f_acts_ = std::make_unique<TierFile>(file_dirs(), stem + "acts.bin", std::max<std::uint64_t>(off, kAlign), direct);
         if (!grad_host_.empty())
-            f_grads_ = std::make_unique<TierFile>(stem + "grads.bin", blocks_ * round_up(param_b), direct);
+            f_grads_ = std::make_unique<TierFile>(file_dirs(), stem + "grads.bin", blocks_ * round_up(param_b), direct);
         // the tier holds the initial states / params before the step
         std::unique_ptr<Device> gen;
         Pinned stage_s, stage_p;
@@ -613,10 +640,10 @@ void Engine::setup() {
                 src_s = stage_s.p;
                 src_p = stage_p.p;
             }
-            IoRequest w{&io_, f_states_->fd(), src_s, round_up(state_b), k * round_up(state_b), true,
+            IoRequest w{&io_, f_states_->stripe(), src_s, round_up(state_b), k * round_up(state_b), true,
                         false, &io_error_, &io_error_text_, &io_mu_};
             run_io(&w);
-            IoRequest wp{&io_, f_params_->fd(), src_p, round_up(param_b), k * round_up(param_b), true,
+            IoRequest wp{&io_, f_params_->stripe(), src_p, round_up(param_b), k * round_up(param_b), true,
                          false, &io_error_, &io_error_text_, &io_mu_};
             run_io(&wp);
         }
@@ -754,7 +781,7 @@ MeasuredRates Engine::calibrate() {
         // a scratch file in the same directory: the tier files already hold
         // the initial states and must not be touched by the probe
         const bool direct = opt_.direct_io && model_.hidden_dim % 64 == 0;
-        TierFile probe_file(opt_.file_dir + "/offsim_" + std::to_string(::getpid()) + "_probe.bin",
+        TierFile probe_file(file_dirs(), "offsim_" + std::to_string(::getpid()) + "_probe.bin",
                             round_up(bytes), direct);
         // the probe buffer joins the registration while it is in use, so the
         // calibrated rates are those of the requests the iteration issues
@@ -771,7 +798,7 @@ MeasuredRates Engine::calibrate() {
                 if (e->io_registered_) e->io_registered_ = e->io_.register_buffers(e->io_bufs_);
             }
         } reregister{this};
-        IoRequest w{&io_, probe_file.fd(), h.p, round_up(bytes), 0, true, false, &io_error_,
+        IoRequest w{&io_, probe_file.stripe(), h.p, round_up(bytes), 0, true, false, &io_error_,
                     &io_error_text_, &io_mu_};
         IoRequest rd = w;
         rd.write = false;
@@ -891,7 +918,7 @@ void* Engine::read_tier_states(std::uint32_t k, Pinned& tmp) {
     const std::uint64_t state_b = 12 * n_;
     if (h_states_[k]) return h_states_[k];  // the host copy the tier was seeded from
     if (!tmp.p) tmp = Pinned(round_up(state_b));
-    IoRequest r{&io_, f_states_->fd(), tmp.p, round_up(state_b), k * round_up(state_b), false, false,
+    IoRequest r{&io_, f_states_->stripe(), tmp.p, round_up(state_b), k * round_up(state_b), false, false,
                 &io_error_, &io_error_text_, &io_mu_};
     run_io(&r);
     if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
@@ -911,7 +938,7 @@ void Engine::write_back_resident() {
         }
         check_cuda(cudaMemcpy(dst, res_states_[k].p, state_b, cudaMemcpyDeviceToHost), "resident write-back");
         if (file_tier_) {
-            IoRequest w{&io_, f_states_->fd(), dst, round_up(state_b), k * round_up(state_b), true, false,
+            IoRequest w{&io_, f_states_->stripe(), dst, round_up(state_b), k * round_up(state_b), true, false,
                         &io_error_, &io_error_text_, &io_mu_};
             run_io(&w);
         }
@@ -929,7 +956,7 @@ std::uint64_t Engine::checksum_states() {
     for (std::uint32_t k = 0; k < blocks_; ++k) {
         const void* src = h_states_[k];
         if (file_tier_) {
-            IoRequest r{&io_, f_states_->fd(), tmp.p, round_up(state_b), k * round_up(state_b), false, false,
+            IoRequest r{&io_, f_states_->stripe(), tmp.p, round_up(state_b), k * round_up(state_b), false, false,
                         &io_error_, &io_error_text_, &io_mu_};
             run_io(&r);
             src = tmp.p;
@@ -986,7 +1013,7 @@ void Engine::issue(const Task& t, ExecReport& rep) {
     };
     auto file = [&](const TierFile& f, void* buf, std::uint64_t bytes, std::uint64_t off, bool write,
                     bool poison) {
-        io_reqs_.push_back(std::make_unique<IoRequest>(IoRequest{&io_, f.fd(), buf, round_up(bytes), off, write,
+        io_reqs_.push_back(std::make_unique<IoRequest>(IoRequest{&io_, f.stripe(), buf, round_up(bytes), off, write,
                                                             poison, &io_error_, &io_error_text_, &io_mu_}));
         check_cuda(cudaLaunchHostFunc(s, run_io, io_reqs_.back().get()), "host io");
         phys(write ? "file_write" : "file_read", bytes);
@@ -1202,7 +1229,10 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
                                        rep.resident_groups);
         add_host_ring_edges(rep.graph, rep.host_ring);
     }
-    if (options.tier == StateTier::file) rep.io_engine = eng.io_engine();
+    if (options.tier == StateTier::file) {
+        rep.io_engine = eng.io_engine();
+        rep.file_devices = static_cast<std::uint32_t>(eng.file_dirs().size());
+    }
     MeasuredRates rates = eng.calibrate();
     rep.io_registered_bytes = eng.io_registered();
     const std::uint64_t cal_fixed = eng.io_fixed(), cal_plain = eng.io_plain();

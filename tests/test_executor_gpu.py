@@ -181,6 +181,13 @@ def test_file_tier_bounded_ring_matches_host_tier(cuda_dev, tmp_path):
         if ring["io_engine"] == "io_uring" and io["registered_bytes"] > 0:
             # every file request's host side is a registered ring slot
             assert io["fixed"] > 0 and io["plain"] == 0, io
+    # striped over three directories (one per SSD): the same states
+    dirs = [str(tmp_path / f"ssd{i}") for i in range(3)]
+    st, striped, _, err = execute(sc, {"tier": "file", "file_dir": dirs, "host_ring": 2,
+                                       "compute_rate": RATE, "checksum_states": True, "seed": 5})
+    assert st == 0, (err, _failing(striped))
+    assert striped["all_invariants_pass"] and striped["swap_mismatches"] == 0
+    assert striped["file_devices"] == 3 and striped["state_checksum"] == host["state_checksum"]
     # registration off: the same result through plain requests
     st, plain, _, err = execute(sc, {"tier": "file", "file_dir": str(tmp_path), "host_ring": 2,
                                      "compute_rate": RATE, "checksum_states": True, "seed": 5,

@@ -54,3 +54,17 @@ def test_io_engine_registered_buffers(tmp_path, mib, depth):
     straddle = mib % 2  # the read buffer's halves meet mid-request for odd MiB
     assert int(kv["plain"]) == straddle
     assert int(kv["fixed"]) == 2 * mib - straddle
+
+
+@pytest.mark.parametrize("count,mib", [(1, 3), (2, 7), (3, 7), (4, 13)])
+def test_io_engine_striped_over_devices(tmp_path, count, mib):
+    """RAID-0 striping over `count` files (the reference's n_ssd devices,
+    hardware.cpp:39-42): a region at an offset that is not unit-aligned
+    round-trips bit-exactly and every device file holds exactly the bytes
+    the mapping assigns it."""
+    if not EXE.exists():
+        pytest.skip("build/io_engine_test not built")
+    r = subprocess.run([str(EXE), str(tmp_path), "stripe", str(count), str(mib)], capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.split()[1:] == ["STRIPE-OK", str(count)]

@@ -142,3 +142,16 @@ def test_resident_groups_move_no_state_bytes(tier, R):
 def test_resident_groups_rejects_bad_value():
     st, _, _, err = execute(C1, {"dry_run": True, "resident_groups": "some"})
     assert st == 2 and "resident_groups" in err
+
+
+def test_file_dir_list_for_striping():
+    """file_dir may list one directory per SSD (tier files striped over
+    them); an empty list or a non-string entry is a config error."""
+    st, s, _, err = execute(C1, {"dry_run": True, "tier": "file", "file_dir": ["/tmp/a", "/tmp/b"]})
+    assert st == 0 and s["all_invariants_pass"], err
+    st, _, _, err = execute(C1, {"dry_run": True, "tier": "file", "file_dir": []})
+    assert st == 2 and "file_dir" in err
+    st, _, _, err = execute(C1, {"dry_run": True, "tier": "file", "file_dir": ["/tmp/a", 3]})
+    assert st == 2
+    st, _, _, err = execute(C1, {"dry_run": True, "tier": "file", "file_dir": ["/tmp/a", "/tmp/a"]})
+    assert st == 2 and "distinct" in err
