@@ -47,10 +47,15 @@ VARIANTS = {
     "lag": (("tma_default", (1, 3, 0), (2048, 0, 0)), ("lag_3stages", (1, 3, 0), (2048, 0, 5)),
             ("lag_4stages", (1, 3, 0), (2048, 0, 6)), ("tma_default_2", (1, 3, 0), (2048, 0, 0)),
             ("lag_3stages_2", (1, 3, 0), (2048, 0, 5)), ("lag_4stages_2", (1, 3, 0), (2048, 0, 6))),
+    # SM budget (fy_adamw_sm_budget): fewer CTAs (one per SM) draw less
+    # power; does the DRAM stay saturated and the clock rise?
+    "budget": tuple((f"sms_{b or 148}{'_2' if rep else ''}", (1, 3, 0), (2048, 0, 0), b)
+                    for rep in (0, 1) for b in (0, 132, 120, 104)),
 }
-for name, tune, bulk in VARIANTS[sys.argv[1] if len(sys.argv) > 1 else "default"]:
+for name, tune, bulk, *budget in VARIANTS[sys.argv[1] if len(sys.argv) > 1 else "default"]:
     check(LIB.fy_adamw_tune(*tune))
     check(LIB.fy_adamw_tune_bulk(*bulk))
+    check(LIB.fy_adamw_sm_budget(budget[0] if budget else 0))
     step()
     torch.cuda.synchronize()
     samples, stop = [], threading.Event()
