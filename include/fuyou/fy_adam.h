@@ -298,7 +298,8 @@ typedef struct fy_swap_config {
     int device;
     uint64_t slot_bytes;  /* SSD ring slot size (0: 64 MiB; rounded to 4 KiB) */
     uint32_t slots;       /* ring slots (0: 4; >= 2)                          */
-    const char* file_dir; /* NULL: /tmp                                       */
+    const char* file_dir; /* NULL: /tmp; "d1:d2:..." = one directory per SSD,
+                             the swap file striped RAID-0 over them (4 MiB) */
     int direct_io;        /* O_DIRECT for the swap file                       */
 } fy_swap_config;
 

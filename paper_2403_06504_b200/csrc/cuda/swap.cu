@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cerrno>
 #include <cstring>
+#include <set>
 
 namespace fy {
 
@@ -29,7 +30,7 @@ void CUDART_CB run_swap_io(void* arg) {
     }
     std::string err;
     try {
-        err = s.engine().transfer(s.fd(), r->buf, r->bytes, r->offset, r->write);
+        err = s.engine().transfer(s.stripe(), r->buf, r->bytes, r->offset, r->write);
     } catch (const std::exception& e) {
         err = e.what();
     }
@@ -48,7 +49,17 @@ Swapper::Swapper(const fy_swap_config& cfg) : cfg_(cfg) {
     if (cfg_.slot_bytes == 0) cfg_.slot_bytes = 64ull << 20;
     if (cfg_.slots < 2) throw ArgError("swapper: slots must be >= 2");
     cfg_.slot_bytes = round_up(cfg_.slot_bytes);
-    dir_ = cfg_.file_dir ? cfg_.file_dir : "/tmp";
+    // one directory, or several separated by ':' (one per SSD: the swap
+    // file is striped RAID-0 over them)
+    const std::string dirs = cfg_.file_dir && *cfg_.file_dir ? cfg_.file_dir : "/tmp";
+    for (std::size_t a = 0; a <= dirs.size();) {
+        const std::size_t b = std::min(dirs.find(':', a), dirs.size());
+        if (b > a) dirs_.push_back(dirs.substr(a, b - a));
+        a = b + 1;
+    }
+    if (dirs_.empty() || dirs_.size() > 64) throw ArgError("swapper: file_dir must name 1..64 directories");
+    if (std::set<std::string>(dirs_.begin(), dirs_.end()).size() != dirs_.size())
+        throw ArgError("swapper: file_dir entries must be distinct");
     try {
         check_cuda(cudaSetDevice(cfg_.device), "cudaSetDevice");
         check_cuda(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "swap d2h stream");
@@ -88,22 +99,36 @@ void Swapper::release_all() noexcept {
     if (h2d_) cudaStreamDestroy(h2d_);
     if (io_s_) cudaStreamDestroy(io_s_);
     d2h_ = h2d_ = io_s_ = nullptr;
-    if (fd_ >= 0) {
-        ::close(fd_);
-        ::unlink(path_.c_str());
-        fd_ = -1;
+    close_files();
+}
+
+void Swapper::close_files() noexcept {
+    for (std::size_t i = 0; i < fds_.size(); ++i) {
+        ::close(fds_[i]);
+        ::unlink(paths_[i].c_str());
     }
+    fds_.clear();
+    paths_.clear();
 }
 
 void Swapper::open_file() {
-    if (fd_ >= 0) return;
-    path_ = dir_ + "/fy_swap_" + std::to_string(::getpid()) + "_" +
-            std::to_string(reinterpret_cast<std::uintptr_t>(this)) + ".bin";
-    int flags = O_RDWR | O_CREAT | O_TRUNC;
-    if (cfg_.direct_io) flags |= O_DIRECT;
-    fd_ = ::open(path_.c_str(), flags, 0600);
-    if (fd_ < 0 && cfg_.direct_io) fd_ = ::open(path_.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
-    if (fd_ < 0) throw DeviceError("swapper: cannot open " + path_ + ": " + std::strerror(errno));
+    if (!fds_.empty()) return;
+    const std::string name = "/fy_swap_" + std::to_string(::getpid()) + "_" +
+                             std::to_string(reinterpret_cast<std::uintptr_t>(this)) + ".bin";
+    for (const std::string& dir : dirs_) {
+        const std::string path = dir + name;
+        int flags = O_RDWR | O_CREAT | O_TRUNC;
+        if (cfg_.direct_io) flags |= O_DIRECT;
+        int fd = ::open(path.c_str(), flags, 0600);
+        if (fd < 0 && cfg_.direct_io) fd = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
+        if (fd < 0) {
+            const std::string why = std::strerror(errno);
+            close_files();
+            throw DeviceError("swapper: cannot open " + path + ": " + why);
+        }
+        fds_.push_back(fd);
+        paths_.push_back(path);
+    }
     // the pinned ring (SSD placement only); all or nothing
     try {
         int dev = 0;
@@ -131,9 +156,7 @@ void Swapper::open_file() {
         slots_.clear();
         slot_free_.clear();
         slot_filled_.clear();
-        ::close(fd_);
-        ::unlink(path_.c_str());
-        fd_ = -1;
+        close_files();
         throw;
     }
 }

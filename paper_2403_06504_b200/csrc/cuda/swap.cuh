@@ -71,14 +71,15 @@ private:
     void* take_host(std::uint64_t bytes, std::uint64_t* cap);
     void give_host(void* p, std::uint64_t cap);
     void open_file();
+    void close_files() noexcept;
     void release_all() noexcept;
 
     fy_swap_config cfg_{};
-    std::string dir_;
+    std::vector<std::string> dirs_; // one per device (striped when > 1)
     cudaStream_t d2h_ = nullptr, h2d_ = nullptr, io_s_ = nullptr;
     IoEngine io_;
-    int fd_ = -1;
-    std::string path_;
+    std::vector<int> fds_;
+    std::vector<std::string> paths_;
     std::uint64_t file_end_ = 0;
     std::vector<void*> slots_;
     std::vector<cudaEvent_t> slot_free_, slot_filled_;
@@ -99,7 +100,9 @@ public:
     std::mutex io_mu;
     std::string io_error;
     IoEngine& engine() { return io_; }
-    int fd() const { return fd_; }
+    IoEngine::Stripe stripe() const {
+        return {fds_.data(), static_cast<unsigned>(fds_.size()), 4ull << 20};
+    }
 };
 
 } // namespace fy

@@ -116,3 +116,36 @@ def test_swap_reports_unusable_swap_dir(cuda_dev):
     sw.sync()
     assert torch.equal(back, t)
     sw.close()
+
+
+def test_swap_ssd_striped_over_directories(cuda_dev, tmp_path):
+    """SSD placement with file_dir = "d0:d1:d2" (one directory per SSD): the
+    swap file is striped RAID-0 over the three in 4 MiB units — every
+    directory holds data, and every buffer comes back byte for byte."""
+    import os
+    from paper_2403_06504_b200 import optim as F
+    from paper_2403_06504_b200._lib import FyError
+    dirs = [tmp_path / f"ssd{i}" for i in range(3)]
+    for d in dirs:
+        d.mkdir()
+    sw = F.Swapper(slot_bytes=8 << 20, slots=3, file_dir=":".join(str(d) for d in dirs))
+    sizes = [4096, (8 << 20) + 4093, 21 << 20, 12345]
+    src = [_pattern(n, 300 + i, cuda_dev) for i, n in enumerate(sizes)]
+    dst = [torch.zeros_like(t) for t in src]
+    torch.cuda.synchronize()
+    handles = [sw.swap_out(t, F.Swapper.SSD) for t in src]
+    sw.sync()
+    for d in dirs:
+        files = list(d.iterdir())
+        assert len(files) == 1 and os.path.getsize(files[0]) > 0, d
+    for h, t in zip(handles, dst):
+        sw.swap_in(h, t)
+    sw.sync()
+    for a, b in zip(src, dst):
+        assert torch.equal(a, b)
+    for h in handles:
+        sw.release(h)
+    sw.close()
+    for bad in (":", f"{dirs[0]}:{dirs[0]}"):
+        with pytest.raises(FyError):
+            F.Swapper(slot_bytes=1 << 20, slots=2, file_dir=bad)
