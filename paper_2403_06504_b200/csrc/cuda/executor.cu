@@ -368,6 +368,7 @@ private:
 
     // file tier
     std::unique_ptr<TierFile> f_states_, f_params_, f_acts_, f_grads_;
+    std::uint64_t tier_states_bytes_ = 0;
     std::vector<std::uint64_t> act_file_off_;
     std::vector<std::uint64_t> ckpt_file_off_;
     std::vector<std::unique_ptr<IoRequest>> io_reqs_;
@@ -604,8 +605,8 @@ void Engine::setup() {
         const bool direct = opt_.direct_io && model_.hidden_dim % 64 == 0;
         const std::string stem = "offsim_" + std::to_string(::getpid()) + "_";
         const bool chunks = has_update_ || has_weights_;
-        f_states_ = std::make_unique<TierFile>(file_dirs(), stem + "states.bin",
-                                               chunks ? blocks_ * round_up(state_b) : kAlign, direct);
+        tier_states_bytes_ = chunks ? blocks_ * round_up(state_b) : kAlign;
+        f_states_ = std::make_unique<TierFile>(file_dirs(), stem + "states.bin", tier_states_bytes_, direct);
         f_params_ = std::make_unique<TierFile>(file_dirs(), stem + "params.bin",
                                                chunks ? blocks_ * round_up(param_b) : kAlign, direct);
         std::uint64_t off = 0;
@@ -823,7 +824,7 @@ MeasuredRates Engine::calibrate() {
         // replay predicted 5.6 GB/s where 75 GB of iteration IO got 4.0)
         constexpr std::uint64_t kReplay = 8ull << 30;
         double rd_b = 0, rd_s = 0, wr_b = 0, wr_s = 0;
-        std::uint64_t wcur = round_up(bytes), written = round_up(bytes), rcur = 0;
+        std::uint64_t wcur = round_up(bytes), written = round_up(bytes), rcur = 0, scur = 0;
         for (const Task& t : g_.tasks) {
             if (t.resource != ResourceId::link_ssd || t.work <= 0.0) continue;
             if (rd_b + wr_b >= double(kReplay)) break;
@@ -836,6 +837,14 @@ MeasuredRates Engine::calibrate() {
                 op.offset = wcur;
                 wcur += b;
                 written = std::max(written, wcur);
+            } else if (f_states_ && tier_states_bytes_ >= b) {
+                // reads come from the real states file (written at setup,
+                // not since), like the iteration's own state reads, rather
+                // than from probe data written a moment before
+                if (scur + b > tier_states_bytes_) scur = 0;
+                op.file = f_states_->stripe();
+                op.offset = scur;
+                scur += b;
             } else {
                 if (rcur + b > written) rcur = 0;
                 op.offset = rcur;
