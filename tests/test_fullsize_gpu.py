@@ -108,3 +108,58 @@ def test_c4_175b_block_sharded_8_equals_single(cuda_dev):
     assert _same_bits(st, single), "sharded states differ from the single launch"
     for r, b in enumerate(full + [local]):
         assert _same_bits(b, p_single), f"rank buffer {r} differs"
+
+
+N_HUGE = (1 << 32) + 3 * 2048 + 5  # one chunk past 2^32 elements (60 GB of states + grads)
+
+
+@pytest.mark.parametrize("path", ["tma", "lsu"])
+def test_chunk_past_2pow32_elements(cuda_dev, path):
+    """Maximum sizes: one launch over a chunk of 2^32 + 6149 elements (no
+    32-bit index may wrap) equals launches over 2^30-element slices of the
+    same inputs bit for bit (Adam is elementwise), and windows straddling
+    2^31 and 2^32 plus the ragged tail equal the CPU oracle."""
+    from paper_2403_06504_b200 import optim as F
+    from paper_2403_06504_b200._lib import LIB, check
+    torch.cuda.empty_cache()  # the other path's 120 GB, still cached by torch
+    free, _ = torch.cuda.mem_get_info(cuda_dev)
+    if free < 135e9:
+        pytest.skip(f"needs ~125 GB of free HBM, {free / 1e9:.0f} GB free")
+    n = N_HUGE
+    check(LIB.fy_adamw_tune(1, 3, 0) if path == "tma" else LIB.fy_adamw_tune(0, 2, 2))
+    try:
+        st, grad = _states(n, cuda_dev, 32)
+        los = (0, (1 << 31) - WINDOW // 2, n - WINDOW)  # the last window straddles 2^32
+        init = {lo: ([st[k * n + lo:k * n + lo + WINDOW].cpu().numpy().copy() for k in range(3)],
+                     grad[lo:lo + WINDOW].cpu().view(torch.int16).numpy().view(np.uint16).copy()) for lo in los}
+        # float64 reference of the grad sum of squares (before the in-place
+        # update overwrites the grads with params), in 2^28-element pieces
+        exp_sq = sum(float(grad[lo:lo + (1 << 28)].double().square().sum()) for lo in range(0, n, 1 << 28))
+        st2, grad2 = st.clone(), grad.clone()
+        hp = F.Hparams(step=7)
+        ws = torch.zeros(F.workspace_floats(), device=cuda_dev)
+        sq1, sq2 = (torch.zeros(1, dtype=torch.float64, device=cuda_dev) for _ in range(2))
+        F.adamw_chunk(st[:n], st[n:2 * n], st[2 * n:], grad, hp, param_out=grad,  # in place
+                      grad_sq_sum=sq1, workspace=ws)
+        piece = 1 << 30
+        for lo in range(0, n, piece):
+            hi = min(n, lo + piece)
+            F.adamw_chunk(st2[lo:hi], st2[n + lo:n + hi], st2[2 * n + lo:2 * n + hi], grad2[lo:hi], hp,
+                          param_out=grad2[lo:hi], grad_sq_sum=sq2, accumulate_sq=lo > 0, workspace=ws)
+        torch.cuda.synchronize()
+        assert _same_bits(st, st2) and _same_bits(grad, grad2)
+        # per-CTA partials are rounded to float once (~6e-8); the per-thread
+        # sums must not drift over 2^32 elements (fp32 running sums: 1.5e-5)
+        for got in (sq1.item(), sq2.item()):
+            assert abs(got - exp_sq) <= 1e-6 * exp_sq, (got, exp_sq)
+        del st2, grad2
+        sc = O.scalars(step=7)
+        for lo, ((mst, mm, vv), g) in init.items():
+            p = np.zeros(WINDOW, np.uint16)
+            O.adamw_step(mst, mm, vv, g, O.BF16, sc, param_out=p)
+            for k, ref in enumerate((mst, mm, vv)):
+                got = st[k * n + lo:k * n + lo + WINDOW].cpu().numpy()
+                assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (lo, k)
+            assert np.array_equal(grad[lo:lo + WINDOW].cpu().view(torch.int16).numpy().view(np.uint16), p), lo
+    finally:
+        check(LIB.fy_adamw_tune(1, 3, 0))
