@@ -65,6 +65,7 @@ struct ExecOptions {
     std::vector<std::string> file_dirs; // >1: tier files striped RAID-0 over these (one per SSD)
     bool direct_io = true;          // O_DIRECT for the file tier
     bool fixed_buffers = true;      // register the staging rings with io_uring (READ/WRITE_FIXED)
+    std::uint32_t io_depth = 32;    // io_uring requests in flight PER tier device (file_dirs entry)
     double compute_rate = 0.0;      // FLOP/s of synthetic compute (0: hw.gpu_tput)
     // fwd/bwd compute tasks: "spin" = timed kernel of work / compute_rate
     // (no SM/HBM contention); "gemm" = the layer's real bf16 GEMMs through

@@ -43,7 +43,7 @@ ParsedOptions parse_options(const char* text) {
                                                "verify_swaps", "adam", "dry_run", "variant",
                                                "swap_only", "max_blocks", "placement",
                                                "compute_mode", "host_ring", "checksum_states",
-                                               "resident_groups", "fixed_buffers"};
+                                               "resident_groups", "fixed_buffers", "io_depth"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -66,6 +66,8 @@ ParsedOptions parse_options(const char* text) {
         }
         o.direct_io = doc.value("direct_io", o.direct_io);
         o.fixed_buffers = doc.value("fixed_buffers", o.fixed_buffers);
+        o.io_depth = doc.value("io_depth", o.io_depth);
+        if (o.io_depth < 1 || o.io_depth > 1024) throw ConfigError("exec options: io_depth must be 1..1024");
         o.compute_rate = doc.value("compute_rate", o.compute_rate);
         o.state_slots = doc.value("state_slots", o.state_slots);
         o.seed = doc.value("seed", o.seed);

@@ -262,7 +262,9 @@ class Engine {
 public:
     Engine(const ModelConfig& model, const SwapPlan& plan, const TaskGraph& mapped,
            const ExecOptions& opt, const std::vector<ChunkBuffers>* chunks)
-        : model_(model), plan_(plan), g_(mapped), opt_(opt), user_(chunks) {}
+        : model_(model), plan_(plan), g_(mapped), opt_(opt), user_(chunks),
+          // one ring for every tier device, io_depth requests in flight on each
+          io_(opt.io_depth * static_cast<unsigned>(std::max<std::size_t>(1, opt.file_dirs.size()))) {}
 
     ~Engine() {
         // drain everything first: host IO callbacks reference io_reqs_ and

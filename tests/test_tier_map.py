@@ -155,3 +155,12 @@ def test_file_dir_list_for_striping():
     assert st == 2
     st, _, _, err = execute(C1, {"dry_run": True, "tier": "file", "file_dir": ["/tmp/a", "/tmp/a"]})
     assert st == 2 and "distinct" in err
+
+
+def test_io_depth_option():
+    """io_depth = io_uring requests in flight per tier device (1..1024)."""
+    st, s, _, err = execute(C1, {"dry_run": True, "tier": "file", "io_depth": 64})
+    assert st == 0, err
+    for bad in (0, 2000):
+        st, _, _, err = execute(C1, {"dry_run": True, "tier": "file", "io_depth": bad})
+        assert st == 2 and "io_depth" in err
