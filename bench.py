@@ -1156,7 +1156,7 @@ def swap_sweep_phase(F, budget_cpu=8e9, budget_ssd=2e9):
     return rows
 
 
-def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True, file_dir="/tmp/offsim_ssd_tier"):
+def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True, file_dir="/tmp/offsim_ssd_tier", io_depth=32):
     """Opt-in (--ssd-tier): one iteration of a 13B-shaped slice whose
     optimizer states live in FILES (O_DIRECT io_uring) and stream through a
     `ring`-slot pinned staging ring — the paper's SSD tier with host memory
@@ -1175,7 +1175,7 @@ def ssd_tier_phase(F, blocks=8, ring=3, fixed_buffers=True, file_dir="/tmp/offsi
     assert L.offsim_scenario_parse(sc.encode(), C.byref(h)) == 0
     summ = P()
     opts = {"tier": "file", "host_ring": ring, "compute_mode": "gemm", "file_dir": file_dir,
-            "fixed_buffers": fixed_buffers}
+            "fixed_buffers": fixed_buffers, "io_depth": io_depth}
     st = L.offsim_execute(h, json.dumps(opts).encode(), C.byref(summ), None)
     L.offsim_scenario_free(h)
     d = json.loads(C.cast(summ, C.c_char_p).value.decode())
