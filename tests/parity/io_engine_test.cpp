@@ -47,7 +47,7 @@ static int faults(const std::string& dir, unsigned depth) {
 // over `count` files with a 1 MiB stripe unit and 256 KiB requests, read back
 // through the engine, and every device file checked against the RAID-0
 // mapping with plain preads. Prints "<engine> STRIPE-OK <count>".
-static int stripe(const std::string& dir, unsigned count, std::uint64_t mib) {
+static int stripe(const std::string& dir, unsigned count, std::uint64_t mib, bool fixed) {
     const std::uint64_t unit = 1ull << 20, bytes = mib << 20, offset = 3 * 4096;
     std::vector<int> fds;
     std::vector<std::string> paths;
@@ -64,6 +64,7 @@ static int stripe(const std::string& dir, unsigned count, std::uint64_t mib) {
     for (std::uint64_t i = 0; i < bytes / 8; ++i) pa[i] = (i + 17) * 0x9e3779b97f4a7c15ull;
     std::memset(b, 0, bytes);
     fy::IoEngine io(8, 256ull << 10);
+    if (fixed) io.register_buffers({{a, bytes}, {b, bytes}});
     const fy::IoEngine::Stripe st{fds.data(), count, unit};
     std::string err = io.transfer(st, a, bytes, offset, true);
     if (err.empty()) err = io.transfer(st, b, bytes, offset, false);
@@ -86,7 +87,9 @@ static int stripe(const std::string& dir, unsigned count, std::uint64_t mib) {
         std::printf("%s STRIPE-MISMATCH %s\n", io.engine(), err.c_str());
         return 1;
     }
-    std::printf("%s STRIPE-OK %u\n", io.engine(), count);
+    std::printf("%s STRIPE-OK %u fixed=%llu plain=%llu\n", io.engine(), count,
+                static_cast<unsigned long long>(io.fixed_requests()),
+                static_cast<unsigned long long>(io.plain_requests()));
     return 0;
 }
 
@@ -94,7 +97,8 @@ int main(int argc, char** argv) {
     if (argc < 3) return 2;
     if (std::string(argv[2]) == "fault") return faults(argv[1], argc > 3 ? std::atoi(argv[3]) : 8);
     if (std::string(argv[2]) == "stripe")
-        return stripe(argv[1], argc > 3 ? std::atoi(argv[3]) : 3, argc > 4 ? std::atoi(argv[4]) : 7);
+        return stripe(argv[1], argc > 3 ? std::atoi(argv[3]) : 3, argc > 4 ? std::atoi(argv[4]) : 7,
+                      argc > 5 && std::string(argv[5]) == "fixed");
     const std::string path = std::string(argv[1]) + "/io_engine_test.bin";
     const std::uint64_t bytes = std::strtoull(argv[2], nullptr, 10) << 20;
     const unsigned depth = argc > 3 ? static_cast<unsigned>(std::atoi(argv[3])) : 32;

@@ -56,15 +56,22 @@ def test_io_engine_registered_buffers(tmp_path, mib, depth):
     assert int(kv["fixed"]) == 2 * mib - straddle
 
 
+@pytest.mark.parametrize("fixed", [False, True])
 @pytest.mark.parametrize("count,mib", [(1, 3), (2, 7), (3, 7), (4, 13)])
-def test_io_engine_striped_over_devices(tmp_path, count, mib):
+def test_io_engine_striped_over_devices(tmp_path, count, mib, fixed):
     """RAID-0 striping over `count` files (the reference's n_ssd devices,
     hardware.cpp:39-42): a region at an offset that is not unit-aligned
     round-trips bit-exactly and every device file holds exactly the bytes
     the mapping assigns it."""
     if not EXE.exists():
         pytest.skip("build/io_engine_test not built")
-    r = subprocess.run([str(EXE), str(tmp_path), "stripe", str(count), str(mib)], capture_output=True,
-                       text=True, timeout=120)
+    args = [str(EXE), str(tmp_path), "stripe", str(count), str(mib)] + (["fixed"] if fixed else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.split()[1:] == ["STRIPE-OK", str(count)]
+    f = r.stdout.split()
+    assert f[1:3] == ["STRIPE-OK", str(count)]
+    kv = dict(x.split("=") for x in f[3:])
+    if f[0] == "io_uring" and fixed and int(kv["fixed"]) > 0:
+        assert int(kv["plain"]) == 0  # every striped request lies inside a registered buffer
+    elif f[0] == "io_uring" and not fixed:
+        assert int(kv["fixed"]) == 0
