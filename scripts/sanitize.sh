@@ -36,4 +36,7 @@ FP32="tma_bulk_path_bit_exact and 14341 and 2- or multi_chunk_launch_bit_exact a
    python -m pytest tests/test_adamw_gpu.py -q -x -k "$FP32" > $OUT/${TAG}_racecheck_fp32.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_racecheck_fp32.log)
 (timeout 900 $CS --tool synccheck --error-exitcode 9 \
    python -m pytest tests/test_adamw_gpu.py -q -x -k "$FP32" > $OUT/${TAG}_synccheck_fp32.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_synccheck_fp32.log)
+# the vectorised grad-stats pass (16-B loads, unaligned / ragged fallbacks)
+(timeout 900 $CS --tool memcheck --error-exitcode 9 \
+   python -m pytest tests/test_adamw_gpu.py -q -x -k "grad_stats or device_side_clipping" > $OUT/${TAG}_memcheck_grad_stats.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_memcheck_grad_stats.log)
 tail -n 3 $OUT/${TAG}_*check*.log
