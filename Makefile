@@ -14,6 +14,19 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(JSONDIR)
 NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -Xptxas -v
 
+# NCCL: the copy torch ships (2.28.x) when present, so a process that also
+# imports torch maps ONE libnccl.so.2; else the system one.
+NCCLDIR  ?= $(shell python3 -c "import os,sysconfig;d=os.path.join(sysconfig.get_paths()['purelib'],'nvidia','nccl');print(d if os.path.isfile(os.path.join(d,'include','nccl.h')) else '')")
+ifneq ($(NCCLDIR),)
+NCCL_INC := -I$(NCCLDIR)/include
+NCCL_LNK := -L$(NCCLDIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCLDIR)/lib
+else
+NCCL_INC :=
+NCCL_LNK := -lnccl
+endif
+LINK_LIBS := -L/usr/local/cuda/lib64 -lcublas -Xlinker -rpath=/usr/local/cuda/lib64 $(NCCL_LNK)
+NVFLAGS  += $(NCCL_INC)
+
 CORE_SRC := $(wildcard $(PKG)/csrc/core/*.cpp)
 CUDA_SRC := $(wildcard $(PKG)/csrc/cuda/*.cu)
 CORE_OBJ := $(patsubst $(PKG)/csrc/core/%.cpp,$(OBJDIR)/core/%.o,$(CORE_SRC))
@@ -21,7 +34,7 @@ CUDA_OBJ := $(patsubst $(PKG)/csrc/cuda/%.cu,$(OBJDIR)/cuda/%.o,$(CUDA_SRC))
 HDRS     := $(wildcard include/offsim/*.hpp include/offsim/*.h include/fuyou/*.h) \
             $(wildcard $(PKG)/csrc/core/*.hpp $(PKG)/csrc/cuda/*.cuh)
 
-all: $(LIBDIR)/liboffsim.so $(if $(CORE_SRC),build/offsim_dump build/io_engine_test build/offsim build/graph_dump) oracle
+all: $(LIBDIR)/liboffsim.so sweep $(if $(CORE_SRC),build/offsim_dump build/io_engine_test build/offsim build/graph_dump) oracle
 
 $(OBJDIR)/core/%.o: $(PKG)/csrc/core/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
@@ -37,11 +50,25 @@ build/liboffsim_core.a: $(CORE_OBJ)
 
 $(LIBDIR)/liboffsim.so.0: $(CORE_OBJ) $(CUDA_OBJ)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -Xlinker -soname=liboffsim.so.0 -o $@ $^ -lpthread \
-	    -L/usr/local/cuda/lib64 -lcublas -Xlinker -rpath=/usr/local/cuda/lib64
+	$(NVCC) $(ARCH) -shared -Xlinker -soname=liboffsim.so.0 -o $@ $^ -lpthread $(LINK_LIBS)
 
 $(LIBDIR)/liboffsim.so: $(LIBDIR)/liboffsim.so.0
 	ln -sf liboffsim.so.0 $@
+
+# Sweep-only build (bench / test tooling, never shipped in $(LIBDIR)): the
+# same library with the TMA kernel's experimental variants compiled in
+# (-DFY_SWEEP_VARIANTS: tile / split-DMA / cache-hint / no-math probes,
+# fy_adamw_tune_bulk). scripts/kernel_sweep.py and the variant test load it.
+SWEEP_SRC := adamw_kernels fy_capi
+SWEEP_OBJ := $(addprefix build/sweep/,$(addsuffix .o,$(SWEEP_SRC)))
+sweep: build/sweep/liboffsim_sweep.so
+
+build/sweep/%.o: $(PKG)/csrc/cuda/%.cu $(HDRS)
+	@mkdir -p build/sweep
+	$(NVCC) $(NVFLAGS) -DFY_SWEEP_VARIANTS -c $< -o $@ 2> build/sweep/$*.ptxas.log || (cat build/sweep/$*.ptxas.log; false)
+
+build/sweep/liboffsim_sweep.so: $(CORE_OBJ) $(filter-out $(addprefix $(OBJDIR)/cuda/,$(addsuffix .o,$(SWEEP_SRC))),$(CUDA_OBJ)) $(SWEEP_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lpthread $(LINK_LIBS)
 
 # Parity driver compiled against this repo's headers + core.
 build/offsim_dump: tests/parity/offsim_dump.cpp build/liboffsim_core.a
@@ -85,4 +112,4 @@ ref:
 clean:
 	rm -rf build $(LIBDIR)
 
-.PHONY: all oracle ref reftests clean
+.PHONY: all oracle ref reftests sweep clean

@@ -35,12 +35,15 @@ buffer becomes the updated bf16 params, task_graph.cpp:493-495).
            predicted), swap_sweep (BASELINE config 5 through the planner),
            swap_engine (fy_swapper_* GB/s), b200_replanning.
 
-N>1 (torchrun): every chunk is sharded across ranks (fy_shard_range, 8-elem
-aligned slices); each rank updates its slice; the updated bf16 slices reach
-every rank through the kernel's fused epilogue (peer stores into a torch
-symmetric-memory buffer over NVLink; `--gather auto`, the default) or an NCCL
-all-gather per chunk (`--gather nccl`, or auto when symmetric memory is
-unavailable) — the only data-path exchange.
+N>1 (torchrun): the step runs through the product's sharded entry point
+(fy_shard_*, one shard per GPU): every chunk is split into 8-aligned slices
+(fy_shard_range); each rank updates its slice and the updated bf16 slices
+reach every rank through the kernel's fused epilogue (peer stores into the
+other ranks' IPC-mapped arenas over NVLink, bootstrapped by the library's own
+NCCL communicator; `--gather auto`, the default) or an in-place NCCL
+all-gather per chunk (`--gather nccl`, or auto when a rank cannot map its
+peers) — the only data-path exchange. NCCL_DEBUG=INFO (subsystem INIT) is
+on at N>1 so the communicator lines (nRanks) are in the log.
 `--impl reference`: times the reference's CPU optimizer path (the oracle port
 of DeepSpeed CPU Adam, all host threads) on rank 0 only.
 """
@@ -95,10 +98,11 @@ def parse():
     ap.add_argument("--shard-blocks", type=int, default=2,
                     help="175B-shaped blocks per step in the streamed-shard phase (0 = skip)")
     ap.add_argument("--no-backward-overlap", action="store_true")
-    ap.add_argument("--gather", choices=["auto", "nccl", "fused"], default="auto",
-                    help="N>1: the kernel's fused peer-store epilogue over symmetric memory "
-                         "(NVLink), or an NCCL all-gather of the bf16 slices; auto = fused "
-                         "when torch symmetric memory rendezvous works, else NCCL (recorded)")
+    ap.add_argument("--gather", choices=["auto", "nccl", "peer", "fused"], default="auto",
+                    help="N>1 (fy_shard gather): the kernel's fused peer-store epilogue into the "
+                         "peers' IPC-mapped arenas (NVLink; 'peer' = 'fused'), or an in-place NCCL "
+                         "all-gather of the bf16 slices; auto = peer unless a rank cannot map its "
+                         "peers, then NCCL on every rank (recorded in config.gather_note)")
     ap.add_argument("--ssd-tier", action="store_true", help="opt-in: file-tier iteration (slow disk)")
     ap.add_argument("--layers", type=int, default=C2["layers"], help="override (debug only)")
     ap.add_argument("--hidden", type=int, default=C2["hidden"], help="override (debug only)")
@@ -189,7 +193,7 @@ def dist_setup(args):
     if same_gpu:
         local = 0
     backend = "gloo" if (same_gpu or args.impl != "b200") else "nccl"
-    if (world > 1 or getattr(args, "gather", "nccl") == "fused") and not dist.is_initialized():
+    if world > 1 and not dist.is_initialized():
         dist.init_process_group(backend, device_id=torch.device("cuda", local) if backend == "nccl" else None)
     return world, rank, local
 
@@ -499,167 +503,137 @@ def streamed_backward_overlap(torch, pipe, chunks, hp, K, P, t_stream):
                         "72*t*h^2 FLOPs/block, separate stream"}
 
 
-def ipc_peer_buffers(F, nbytes, world, rank):
-    """Every rank allocates its full-param buffer with fy_ipc_alloc and
-    publishes the CUDA IPC handle; each rank opens the others' handles.
-    Returns {"ptrs": [device pointer of rank q's buffer as seen here]}."""
+def group_nccl_id(F, world, rank):
+    """rank 0's fy_nccl_unique_id, broadcast over the torch.distributed group
+    (out-of-band bootstrap of the library's own communicator)."""
     import torch.distributed as dist
-    own = C.c_void_p()
-    handle = (C.c_char * 64)()
-    F.check(F.LIB.fy_ipc_alloc(nbytes, C.byref(own), handle))
-    handles = [None] * world
-    dist.all_gather_object(handles, bytes(handle))
-    ptrs = []
-    for q in range(world):
-        if q == rank:
-            ptrs.append(own.value)
-            continue
-        p = C.c_void_p()
-        hq = (C.c_char * 64).from_buffer_copy(handles[q])
-        F.check(F.LIB.fy_ipc_open(hq, C.byref(p)))
-        ptrs.append(p.value)
-    return {"ptrs": ptrs, "own": own}
+    obj = [F.optim.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def make_shard(torch, F, args, world, rank, local, sizes, tier, prefer, **kw):
+    """fy_shard_create on every rank; at N>1 the PEER gather (fused epilogue
+    over IPC-mapped arenas bootstrapped through NCCL) unless a rank cannot
+    map its peers, then all ranks fall back to the NCCL all-gather together
+    (the decision is collective, so no rank is left waiting)."""
+    note = None
+    if world == 1:
+        return F.optim.Shard(sizes, device=local, tier=tier, **kw), None, note
+    import torch.distributed as dist
+    gather = prefer
+    sh, err = None, None
+    same_gpu = os.environ.get("FY_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        gather = "peer"
+    try:
+        if gather == "peer" and same_gpu:
+            # test hook (several ranks on one GPU): NCCL refuses that, so the
+            # arenas' IPC handles travel over the gloo group instead
+            sh = F.optim.Shard(sizes, world=world, rank=rank, device=local, gather="peer", tier=tier, **kw)
+            handles = [None] * world
+            dist.all_gather_object(handles, sh.ipc_handle())
+            sh.connect(handles)
+        else:
+            sh = F.optim.Shard(sizes, world=world, rank=rank, device=local, gather=gather,
+                               nccl_id=group_nccl_id(F, world, rank), tier=tier, **kw)
+    except Exception as e:  # noqa: BLE001
+        err = str(e)
+    if max_over_ranks(0.0 if sh is not None else 1.0, world) == 0.0:
+        return sh, gather, note
+    if sh is not None:
+        sh.close()
+    if gather == "nccl":
+        raise RuntimeError(f"fy_shard_create failed: {err}")
+    note = f"PEER gather unavailable ({(err or 'another rank')[:160]}); NCCL all-gather"
+    sh = F.optim.Shard(sizes, world=world, rank=rank, device=local, gather="nccl",
+                       nccl_id=group_nccl_id(F, world, rank), tier=tier, **kw)
+    return sh, "nccl", note
 
 
 def resident_phase(torch, F, args, world, rank, local):
-    """The headline: device-resident step (value + roofline) and its e2e."""
-    import torch.distributed as dist
+    """The headline: the device-resident step through the product's sharded
+    entry point (fy_shard_*; N=1: one shard, no gather) — value + roofline —
+    and its e2e."""
     L, N = args.layers, 12 * args.hidden * args.hidden
     P = L * N
-    off, cnt = F.optim.shard_range(N, world, rank, 8)
-    slice_pad = (-(-N // world) + 7) // 8 * 8
     dev = torch.device("cuda", local)
+    prefer = "nccl" if args.gather == "nccl" else "peer"
+    sh, gather, note = make_shard(torch, F, args, world, rank, local, [N] * L, "device", prefer)
+    sl = [sh.slice(k) for k in range(L)]
+    cnt = sl[0]["count"]
     gen = torch.Generator(device=dev)
     states, grads = [], []
     for k in range(L):
         gen.manual_seed(SEED + k)
-        st = torch.empty(3 * slice_pad, dtype=torch.float32, device=dev)
-        st[:cnt].normal_(0, 0.02, generator=gen)
-        st[slice_pad:slice_pad + cnt].normal_(0, 1e-3, generator=gen)
-        st[2 * slice_pad:2 * slice_pad + cnt].normal_(0, 1e-3, generator=gen).square_()
-        g = (torch.randn(slice_pad, device=dev, generator=gen) * 1e-3).to(torch.bfloat16)
+        c = sl[k]["count"]
+        st = torch.empty(3 * c, dtype=torch.float32, device=dev)
+        st[:c].normal_(0, 0.02, generator=gen)
+        st[c:2 * c].normal_(0, 1e-3, generator=gen)
+        st[2 * c:].normal_(0, 1e-3, generator=gen).square_()
         states.append(st)
-        grads.append(g)
-    full = None
-    fused = args.gather == "fused" or (args.gather == "auto" and world > 1)
-    gather_note = None
-    dst_ptrs = None
-    symm = None
-    if fused:
-        # one symmetric buffer holding every chunk's full bf16 params on
-        # every rank; rank r's slice of chunk k starts at (k*world + r)*pad
-        try:
-            import torch.distributed._symmetric_memory as symm_mem
-            big = symm_mem.empty(L * world * slice_pad, dtype=torch.bfloat16, device=dev)
-            symm = symm_mem.rendezvous(big, dist.group.WORLD.group_name)
-            full = [big[k * world * slice_pad:(k + 1) * world * slice_pad] for k in range(L)]
-            dst_ptrs = [[symm.buffer_ptrs[q] + 2 * (k * world + rank) * slice_pad
-                         for q in range(world)] for k in range(L)]
-        except Exception as e:
-            torch.cuda.empty_cache()
-            symm = None
-            if world > 1:
-                # the same peer-store epilogue on CUDA IPC buffers (fy_ipc_*),
-                # with a host barrier per step instead of the device one
-                try:
-                    ipc = ipc_peer_buffers(F, L * world * slice_pad * 2, world, rank)
-                    dst_ptrs = [[ipc["ptrs"][q] + 2 * (k * world + rank) * slice_pad for q in range(world)]
-                                for k in range(L)]
-                    gather_note = f"symmetric memory unavailable ({str(e)[:120]}); fused epilogue over CUDA IPC"
-                except Exception as e2:  # the NCCL all-gather instead (a device path too)
-                    if args.gather == "fused":
-                        raise
-                    fused, gather_note = False, f"no peer buffers ({str(e)[:80]}; {str(e2)[:80]}); NCCL"
-            elif args.gather == "fused":
-                raise
-            else:
-                fused = False
-    if world > 1 and not fused:
-        full = [torch.empty(world * slice_pad, dtype=torch.bfloat16, device=dev) for _ in range(L)]
-    ws = torch.zeros(F.optim.workspace_floats(), device=dev)
-    sq = torch.zeros(1, dtype=torch.float64, device=dev)
-    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        grads.append((torch.randn(c, device=dev, generator=gen) * 1e-3).to(torch.bfloat16))
+    io = [dict(states=states[k].data_ptr(), grad=grads[k].data_ptr()) for k in range(L)]
     stream = torch.cuda.current_stream(dev)
-    comm = torch.cuda.Stream(dev) if world > 1 else None
     hp = F.optim.Hparams()
+    sq_last = [0.0, 0]
 
-    def one_step(step_idx, evs=None):
+    def one_step(step_idx, upd=None):
         hp.step = 10 + step_idx
-        for k in range(L):
-            st = states[k]
-            if evs is not None:
-                evs[k][0].record(stream)
-            if fused:  # update + all-gather in one kernel (peer stores)
-                F.optim.adamw_chunk_gather(st[:slice_pad], st[slice_pad:2 * slice_pad],
-                                           st[2 * slice_pad:], grads[k], hp, grads[k], dst_ptrs[k],
-                                           grad_sq_sum=sq, workspace=ws, stream=stream, n=cnt)
-            else:
-                F.optim.adamw_chunk(st[:slice_pad], st[slice_pad:2 * slice_pad],
-                                    st[2 * slice_pad:], grads[k], hp, param_out=grads[k],
-                                    grad_sq_sum=sq, accumulate_sq=k > 0, workspace=ws,
-                                    nonfinite=bad, stream=stream, n=cnt)
-            if evs is not None:
-                evs[k][1].record(stream)
-            if world > 1 and not fused:
-                done = torch.cuda.Event()
-                done.record(stream)
-                comm.wait_event(done)
-                with torch.cuda.stream(comm):
-                    dist.all_gather_into_tensor(full[k], grads[k])
-        if world > 1 and not fused:
-            stream.wait_stream(comm)
-        if fused and symm is not None:
-            with torch.cuda.stream(stream):
-                symm.barrier(channel=0)  # peers' stores landed before the params are used
-        elif fused and world > 1:
-            torch.cuda.synchronize()     # IPC buffers: host barrier per step
-            dist.barrier()
+        sh.step(io, hp, want_grad_norm=True, stream=stream)
+        if upd is not None:  # per-chunk kernel times (events on the shard's update stream)
+            sq_last[:] = sh.wait()
+            upd.extend(sh.update_ms())
 
     for w in range(args.warmup):
         one_step(w)
+        sh.wait()
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-            for _ in range(L)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
+    launch_ms = []
     t_start.record(stream)
     for s in range(args.steps):
-        one_step(args.warmup + s, evs[s])
+        one_step(args.warmup + s, launch_ms)
     t_end.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
     clocks = sampler.stop() if rank == 0 else None
-    ms_total = t_start.elapsed_time(t_end)
-    ms_total = max_over_ranks(ms_total, world)
-    launch_ms = [evs[s][k][0].elapsed_time(evs[s][k][1]) for s in range(args.steps) for k in range(L)]
+    ms_total = max_over_ranks(t_start.elapsed_time(t_end), world)
+    stats = sh.stats()
+    launch_ms = [x for x in launch_ms if x > 0]
     mean_launch_s = statistics.mean(launch_ms) * 1e-3
+    peer_kernels = 2 if gather == "peer" else 0  # entry + exit device barriers per step
     res = {
         "ms_per_step": ms_total / args.steps,
         "value": args.steps * P / (ms_total * 1e-3),
         "launch_ms_mean": statistics.mean(launch_ms),
         "launch_ms_p50": statistics.median(launch_ms),
-        "kernel_share": sum(launch_ms) / ms_total,
+        "kernel_share": sum(launch_ms) / t_start.elapsed_time(t_end),
         "params_per_launch": cnt,
         "mean_launch_s": mean_launch_s,
         "clocks": clocks,
-        "launches": args.steps * L * 2,  # fused Adam kernel + 1-block ordered norm reduction
-        "grad_sq_sum": float(sq.item()),
-        "nonfinite": int(bad.item()),
-        "gather": (("fused-ipc" if symm is None and world > 1 else "fused") if fused else "nccl")
-                  if world > 1 or fused else None,
-        "gather_note": gather_note,
+        # fused Adam kernel + 1-block ordered norm reduction per chunk (+ barriers)
+        "launches": args.steps * (L * 2 + peer_kernels),
+        "grad_sq_sum": sq_last[0],
+        "nonfinite": sq_last[1],
+        "gather": gather,
+        "gather_note": note,
+        "entry_point": "fy_shard_step (C ABI; one shard per GPU)",
+        "gather_bytes_per_rank_per_step": stats["gather_bytes"],
+        "tma_stages": stats["stages"],
     }
-
     if world == 1:
-        # the same step as ONE multi-chunk launch (fy_adamw_chunks), beside
-        # the per-chunk headline (reported, not the headline)
-        multi = [(st[:slice_pad], st[slice_pad:2 * slice_pad], st[2 * slice_pad:], grads[k], grads[k])
-                 for k, st in enumerate(states)]
+        # the same step as ONE fy_adamw_chunks call, beside the headline
+        multi = [(st[:cnt], st[cnt:2 * cnt], st[2 * cnt:], grads[k], grads[k]) for k, st in enumerate(states)]
+        ws = torch.zeros(F.optim.workspace_floats(), device=dev)
+        sq = torch.zeros(1, dtype=torch.float64, device=dev)
+        bad = torch.zeros(1, dtype=torch.int32, device=dev)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         F.optim.adamw_chunks(multi, hp, grad_sq_sum=sq, workspace=ws, nonfinite=bad)
         torch.cuda.synchronize()
@@ -675,61 +649,66 @@ def resident_phase(torch, F, args, world, rank, local):
                               "launches_per_step": (2 * L if N // 2048 >= 16384 else 2 * (-(-L // 96))),
                               "note": "fy_adamw_chunks over the 40 chunks; chunks this large keep one "
                                       "launch each inside the call (profiles/r01z_multi_chunk_ab.txt)"}
+    sh.close()
+    del io
     if not args.no_e2e:
-        res["e2e"] = e2e_phase(torch, F, args, states, slice_pad, cnt, world, full)
-    del states, grads, full
+        res["e2e"] = e2e_phase(torch, F, args, states, cnt, world, rank, local)
+    del states, grads
     torch.cuda.empty_cache()
     return res
 
 
-def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
-    """Same step through fy_pipeline_* with host grads in / host params out.
-    N>1: each rank streams its own slice (padded to slice_pad) and the
-    updated bf16 slices are all-gathered on the device after each step; the
-    time is the max over ranks."""
+def e2e_phase(torch, F, args, states, cnt, world, rank, local):
+    """Same step through fy_pipeline_* with host grads in / host params out
+    (states of this rank's slice resident in HBM). N>1: each rank streams its
+    own slice; the kernel also writes the slice into the block's full-param
+    buffer on the device and the block's NCCL all-gather starts on a side
+    stream as soon as the block is updated (fy_chunk.update_done), overlapping
+    the next blocks' host-link traffic. Time: host wall clock, max over
+    ranks."""
     import torch.distributed as dist
     L = len(states)
-    n = slice_pad
-    # the link's duplex rate right before this phase (host links drift over a
-    # run): the denominator of the e2e roofline
+    n = cnt
+    pad = (n + 7) // 8 * 8
     link_now = pcie_peaks(torch) if world == 1 else None
-    if world > 1 and full is None:  # IPC-gather runs keep no torch-side full buffers
-        full = [torch.empty(world * n, dtype=torch.bfloat16, device="cuda") for _ in range(L)]
+    dev = torch.device("cuda", local)
+    full = [torch.empty(world * pad, dtype=torch.bfloat16, device=dev) for _ in range(L)] if world > 1 else None
     hbuf = []
+    rng = np.random.default_rng(SEED + 77 + rank)
     for k in range(L):
         p = C.c_void_p()
         F.check(F.LIB.fy_host_alloc(2 * n, C.byref(p)))
         hbuf.append(p)
-    # initial host grads: bf16 ~ 1e-3 (0x3A83)
+    # host grads: bf16 of N(0, 1e-3^2) (SURVEY §8d), one pattern reused per block
+    pattern = torch.from_numpy(rng.normal(0, 1e-3, min(n, 1 << 24)).astype(np.float32)).to(
+        torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     for p in hbuf:
         arr = np.ctypeslib.as_array((C.c_uint16 * n).from_address(p.value))
-        arr[:] = 0x3A83
-    # N>1: the kernel also writes this rank's params into its own slice of
-    # the chunk's full-param buffer on the device, and an in-place NCCL
-    # all-gather assembles the rest (no extra host round trip)
-    rank = dist.get_rank() if world > 1 else 0
-    # each block is fed to the pipeline as E2E_PIECES units (8-aligned; the
-    # SoA states stay where they are, fy_chunk.states_stride = slice); whole
-    # blocks measured best (profiles/r01ae_e2e_shape_ab.txt)
-    bounds = [min(n, (n * q // E2E_PIECES + 7) // 8 * 8) for q in range(E2E_PIECES)] + [n]
-    spans = [(a, b) for a, b in zip(bounds, bounds[1:]) if b > a]
-    pipe = F.optim.ChunkPipeline(max(b - a for a, b in spans), slots=4, grads_on_host=True,
-                                 params_to_host=True, keep_params_on_device=world > 1,
-                                 states_on_device=True)
-    chunks = [dict(n=b - a, h_states=states[k].data_ptr() + 4 * a, states_stride=n,
-                   grad=hbuf[k].value + 2 * a, h_param=hbuf[k].value + 2 * a,
-                   d_param=full[k][rank * n + a:rank * n + b].data_ptr() if world > 1 else None)
-              for k in range(L) for a, b in spans]
+        for a in range(0, n, pattern.size):
+            arr[a:a + pattern.size] = pattern[:n - a]
+    done = [torch.cuda.Event() for _ in range(L)]
+    pipe = F.optim.ChunkPipeline(n, slots=4, grads_on_host=True, params_to_host=True,
+                                 keep_params_on_device=world > 1, states_on_device=True)
+    chunks = [dict(n=n, h_states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value,
+                   d_param=full[k][rank * pad:rank * pad + n].data_ptr() if world > 1 else None,
+                   update_done=done[k].cuda_event if world > 1 else None)
+              for k in range(L)]
+    for e in done:
+        e.record()  # create the events before the pipeline records into them
+    comm = torch.cuda.Stream(dev) if world > 1 else None
     hp = F.optim.Hparams()
 
     def step(i):
         hp.step = i
         pipe.step(chunks, hp, want_grad_norm=True)
-        pipe.wait()
-        if world > 1:  # assemble the full bf16 params on every rank (NVLink)
+        if world > 1:  # per block, as soon as it is updated (overlaps the host link)
             for k in range(L):
-                dist.all_gather_into_tensor(full[k], full[k][rank * n:(rank + 1) * n])
-            torch.cuda.synchronize()
+                comm.wait_event(done[k])
+                with torch.cuda.stream(comm):
+                    dist.all_gather_into_tensor(full[k], full[k][rank * pad:(rank + 1) * pad])
+        pipe.wait()
+        if world > 1:
+            comm.synchronize()
 
     for w in range(args.warmup):
         step(1000 + w)
@@ -743,6 +722,7 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
     pipe.close()
     for p in hbuf:
         F.check(F.LIB.fy_host_free(p))
+    del full
     P = args.layers * 12 * args.hidden * args.hidden  # whole-job params per step
     return {
         "value": args.steps * P / el, "unit": UNIT,
@@ -751,36 +731,64 @@ def e2e_phase(torch, F, args, states, slice_pad, cnt, world, full):
         "link_gbs_each_way": 2 * L * n * args.steps / el / 1e9,
         "path": "fy_pipeline_step (C ABI): host bf16 grads H2D -> fused AdamW on HBM-resident "
                 "states -> bf16 params D2H into the same host buffer; wall clock"
-                + ("; + in-place NCCL all-gather of the device-side bf16 slices" if world > 1 else ""),
-        "launches": args.steps * len(chunks) * 2,
-        "pieces_per_block": len(spans),
+                + ("; + per-block NCCL all-gather of the device-side bf16 slices, overlapped "
+                   "(fy_chunk.update_done)" if world > 1 else ""),
+        "launches": args.steps * L * 2,
+        "grads": "bf16 of N(0, 1e-3^2) (SURVEY.md §8d)",
         "pcie_at_e2e": link_now,
     }
 
 
-def streamed_shard_phase(torch, F, args, world, rank, local, duplex_gbs=None):
-    """BASELINE config 4's regime: GPT-3-175B-shaped blocks (1,811,939,328
-    params) with master/m/v streamed from each rank's NUMA-local pinned host
-    memory. Every block is sharded across the ranks (fy_shard_range); each
-    rank streams its slice as 4 strided pipeline pieces (12 B/param H2D,
-    12 B/param states + 2 B/param bf16 params D2H, grads in HBM) and also
-    keeps its updated bf16 slice on the device, inside the block's full-param
-    buffer; at N>1 an NCCL all-gather of each block starts on a side stream
-    as soon as the block's last piece is updated (fy_chunk.update_done), so
-    the NVLink traffic overlaps the next block's streaming. `args.shard_blocks`
-    blocks per step (host memory bounds the sample). value = whole-job params
-    per second over the max-over-ranks step time (host clock, both sides
-    synchronised)."""
+def link_probe(torch, world, rank):
+    """Host-link peaks for the streamed regime at this N: every rank's link
+    measured ALONE (ranks take turns) and all ranks' links at once (the
+    aggregate exposes a shared host-DRAM / PCIe-switch cap). Returns rank 0's
+    view: per-rank solo and concurrent GB/s and the aggregates."""
+    solo = None
+    for r in range(world):
+        barrier(world)
+        if r == rank:
+            solo = pcie_peaks(torch)
+        barrier(world)
+    barrier(world)
+    conc = pcie_peaks(torch) if world > 1 else solo
+    if world == 1:
+        return {"per_rank_solo": [solo], "per_rank_concurrent": [solo],
+                "sum_solo_duplex_each_gbs": solo["duplex_each_gbs"],
+                "concurrent_duplex_each_gbs": solo["duplex_each_gbs"]}
     import torch.distributed as dist
+    allp = [None] * world
+    dist.all_gather_object(allp, (solo, conc))
+    return {"per_rank_solo": [a for a, _ in allp], "per_rank_concurrent": [b for _, b in allp],
+            "sum_solo_duplex_each_gbs": sum(a["duplex_each_gbs"] for a, _ in allp),
+            "concurrent_duplex_each_gbs": sum(b["duplex_each_gbs"] for _, b in allp),
+            "note": "concurrent = every rank's 1 GiB H2D+D2H at once (host DRAM / switch cap)"}
+
+
+def streamed_shard_phase(torch, F, args, world, rank, local):
+    """BASELINE config 4's regime through the product's sharded entry point
+    (fy_shard_*, FY_TIER_HOST): GPT-3-175B-shaped blocks (1,811,939,328
+    params) whose master/m/v live in each rank's NUMA-local pinned host
+    memory (fy_host_alloc). Every block is sharded across the ranks; each
+    rank streams its slice through the library's chunk pipeline as 4 strided
+    pieces (12 B/param H2D, 12 B/param states + 2 B/param bf16 params D2H,
+    grads in HBM) and the block's NCCL all-gather of the updated bf16 params
+    runs on the shard's comm stream as soon as the block is updated,
+    overlapping the next block's streaming. `args.shard_blocks` blocks per
+    step (host RAM bounds the sample). value = whole-job params/s over the
+    max-over-ranks device step time (fy_shard events)."""
     N4 = 12 * 12288 * 12288
     K = args.shard_blocks
-    P = 4
-    off, cnt = F.optim.shard_range(N4, world, rank, 8)
-    pad = (-(-N4 // world) + 7) // 8 * 8
+    links = link_probe(torch, world, rank)
     dev = torch.device("cuda", local)
-    bounds = [min(cnt, (cnt * q // P + 7) // 8 * 8) for q in range(P)] + [cnt]
-    spans = [(a, b) for a, b in zip(bounds, bounds[1:]) if b > a]
-    ptrs, desc, grads, fulls, done = [], [], [], [], []
+    sizes = [N4] * K
+    pieces = 4
+    probe = F.optim.shard_range(N4, world, rank, 8)[1]
+    piece = max(8, (-(-probe // pieces) + 7) // 8 * 8)
+    sh, gather, note = make_shard(torch, F, args, world, rank, local, sizes, "host", "nccl",
+                                  slots=4, piece_elems=piece, params_to_host=True)
+    cnt = sh.slice(0)["count"]
+    ptrs, io, grads = [], [], []
     gen = torch.Generator(device=dev)
     for k in range(K):
         hst, hpar = C.c_void_p(), C.c_void_p()
@@ -794,55 +802,45 @@ def streamed_shard_phase(torch, F, args, world, rank, local, duplex_gbs=None):
             host[r * cnt:(r + 1) * cnt].copy_(t.square_() if sqr else t)
             del t
         grads.append((torch.randn(cnt, device=dev, generator=gen) * 1e-3).to(torch.bfloat16))
-        fulls.append(torch.empty(world * pad, dtype=torch.bfloat16, device=dev))
-        ev = torch.cuda.Event()
-        ev.record()
-        done.append(ev)
-        for j, (a, b) in enumerate(spans):
-            d = dict(n=b - a, h_states=hst.value + 4 * a, states_stride=cnt,
-                     grad=grads[k].data_ptr() + 2 * a, h_param=hpar.value + 2 * a,
-                     d_param=fulls[k][rank * pad + a:rank * pad + b].data_ptr())
-            if j == len(spans) - 1:
-                d["update_done"] = ev.cuda_event
-            desc.append(d)
+        io.append(dict(states=hst.value, grad=grads[k].data_ptr(), h_param=hpar.value))
     torch.cuda.synchronize()
-    pipe = F.optim.ChunkPipeline(max(b - a for a, b in spans), slots=4, params_to_host=True,
-                                 keep_params_on_device=True)
-    comm = torch.cuda.Stream(dev) if world > 1 else None
     hp = F.optim.Hparams()
 
     def step(i):
         hp.step = 10 + i
-        pipe.step(desc, hp)
-        if world > 1:
-            for k in range(K):
-                comm.wait_event(done[k])
-                with torch.cuda.stream(comm):
-                    dist.all_gather_into_tensor(fulls[k], fulls[k][rank * pad:(rank + 1) * pad])
-        pipe.wait()
-        torch.cuda.synchronize()
+        sh.step(io, hp)
+        sh.wait()
+        return sh.stats()["step_ms"]
 
     step(0)
     barrier(world)
     reps = 2
     t0 = time.perf_counter()
-    for i in range(reps):
-        step(1 + i)
-    el = max_over_ranks((time.perf_counter() - t0) / reps, world)
-    pipe.close()
+    dev_ms = [step(1 + i) for i in range(reps)]
+    wall = max_over_ranks((time.perf_counter() - t0) / reps, world)
+    el = max_over_ranks(statistics.mean(dev_ms) * 1e-3, world)
+    upd_ms = sum(sh.update_ms())
+    st = sh.stats()
+    sh.close()
     for p in ptrs:
         F.check(F.LIB.fy_host_free(p))
-    del grads, fulls
+    del grads
     torch.cuda.empty_cache()
-    d2h_gbs = 14 * cnt * K / el / 1e9  # this rank's binding direction
-    out = {"value": K * N4 / el, "unit": UNIT, "blocks_per_step": K, "block_params": N4,
-           "params_per_rank": cnt * K, "step_s": el, "per_rank_d2h_gbs": d2h_gbs,
-           "gather": "NCCL all-gather per block on a side stream, gated on update_done" if world > 1 else None,
-           "scaling": "strong (fixed blocks, sliced across ranks)"}
-    if duplex_gbs:
-        out["roofline"] = {"bound": "per-rank host-link D2H", "achieved": d2h_gbs, "peak": duplex_gbs,
-                           "unit": "GB/s", "frac": d2h_gbs / duplex_gbs}
-    return out
+    d2h_total = 14 * N4 * K / el / 1e9        # whole job, the binding direction
+    h2d_total = 12 * N4 * K / el / 1e9
+    peak = min(links["sum_solo_duplex_each_gbs"], links["concurrent_duplex_each_gbs"])
+    return {"value": K * N4 / el, "unit": UNIT, "blocks_per_step": K, "block_params": N4,
+            "params_per_rank": cnt * K, "step_s_device": el, "step_s_wall": wall,
+            "d2h_gbs_whole_job": d2h_total, "h2d_gbs_whole_job": h2d_total,
+            "update_ms_per_step_rank0": upd_ms,
+            "entry_point": "fy_shard_step (C ABI), FY_TIER_HOST",
+            "gather": gather, "gather_note": note,
+            "gather_bytes_per_rank_per_step": st["gather_bytes"],
+            "links": links,
+            "roofline": {"bound": "host links, D2H (14 B/param) — min(sum of per-rank solo duplex, "
+                                  "all ranks concurrently)",
+                         "achieved": d2h_total, "peak": peak, "unit": "GB/s", "frac": d2h_total / peak},
+            "scaling": "strong (fixed blocks, sliced across ranks)"}
 
 
 def configs_phase(torch, F, args):
@@ -1298,6 +1296,10 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # communicator lines (rank / nRanks / nNodes) for the log; INIT only
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     world, rank, local = dist_setup(args)
     torch.cuda.set_device(local)
@@ -1358,8 +1360,7 @@ def main():
                 extra["swap_engine"] = f"failed: {e}"
     if args.shard_blocks > 0 and not args.no_streamed:
         try:
-            extra["streamed_shard"] = streamed_shard_phase(
-                torch, F, args, world, rank, local, (pcie or {}).get("duplex_each_gbs"))
+            extra["streamed_shard"] = streamed_shard_phase(torch, F, args, world, rank, local)
         except Exception as e:  # evidence only; never masks the headline
             extra["streamed_shard"] = f"failed: {e}"
             torch.cuda.empty_cache()
@@ -1424,10 +1425,11 @@ def main():
     if cpu is not None:
         line["cpu_baseline"] = cpu
     line.update(extra)
-    print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1:  # tear down first: the JSON line is the last thing printed
         import torch.distributed as dist
         dist.destroy_process_group()
+    sys.stdout.flush()
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

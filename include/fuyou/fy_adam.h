@@ -50,12 +50,16 @@ const char* fy_version(void);
 const char* fy_last_error(void);
 
 /* Adam hyper-parameters of one step. Semantics: DeepSpeed 0.9.3
- * DeepSpeedCPUAdam (the optimizer the paper runs):
- * bias_correction1 = 1 - beta1^step, bias_correction2 = 1/sqrt(1-beta2^step)
- * (beta^step evaluated in double, stored float), eps added after the
+ * DeepSpeedCPUAdam (the optimizer the paper runs),
+ * csrc/includes/cpu_adam.h update_state: bias_correction1 = 1 - beta1^t,
+ * bias_correction2 = 1 / sqrtf(1 - beta2^t) (float ops), eps added after the
  * bias-corrected sqrt(v), decoupled decay when adamw_mode != 0. The gradient
  * is first multiplied by grad_scale (1/loss_scale, times a clip coefficient
- * if the caller clips). */
+ * if the caller clips).
+ * beta^t: beta_t_given == 0 -> float(pow(double(beta), step)), the value a
+ * fresh DeepSpeed optimizer or a step-number jump produces; beta_t_given != 0
+ * -> beta1_t / beta2_t as given, e.g. by fy_adam_counter_next, which keeps
+ * DeepSpeed's running product across consecutive calls. */
 typedef struct fy_adam_hparams {
     float lr;
     float beta1;
@@ -66,7 +70,29 @@ typedef struct fy_adam_hparams {
     int adamw_mode;
     int bias_correction;
     float grad_scale;
+    int beta_t_given;
+    float beta1_t;
+    float beta2_t;
 } fy_adam_hparams;
+
+/* DeepSpeed's per-optimizer step bookkeeping (cpu_adam.h Adam_Optimizer::
+ * IncrementStep, run once per adam_update call = once per parameter chunk):
+ * with unchanged betas and a step number one past the counter's, beta^t is
+ * the float running product beta_t *= beta; otherwise (first call of a step
+ * whose chunk 0 already advanced the counter, a restart, changed betas)
+ * beta^t = float(pow(double(beta), step)). So in a step over K chunks, chunk
+ * 0 takes fl(beta^(t-1) * beta) and chunks 1..K-1 take pow — bit for bit
+ * what DeepSpeedCPUAdam hands its kernel. init = the optimizer's constructor
+ * (step 0, beta^0 = 1). next: IncrementStep(hp->step, hp->beta1, hp->beta2),
+ * then writes hp->beta1_t / beta2_t and sets hp->beta_t_given. */
+typedef struct fy_adam_counter {
+    uint64_t step;
+    float beta1, beta2;
+    float beta1_t, beta2_t;
+    int constructed; /* 0: constructed lazily with the first call's betas */
+} fy_adam_counter;
+fy_status fy_adam_counter_init(fy_adam_counter* c, float beta1, float beta2);
+fy_status fy_adam_counter_next(fy_adam_counter* c, fy_adam_hparams* hp);
 
 /* One chunk (one transformer block = 12h^2 params, or a shard slice of it).
  * master / exp_avg / exp_avg_sq: fp32 [n] device pointers, updated in place.
@@ -105,16 +131,21 @@ typedef struct fy_adamw_args {
 uint32_t fy_adamw_workspace_floats(void);
 
 /* Fused unscale + grad-norm partial + AdamW + downcast, one launch (two when
- * grad_sq_sum is requested: the second is a one-block ordered reduction). */
+ * grad_sq_sum is requested: the second is a one-block ordered reduction).
+ * n == 0, or a launch skipped by *skip_if_set, contributes 0 to grad_sq_sum
+ * (written as 0 when accumulate_sq == 0). */
 fy_status fy_adamw_chunk(const fy_adamw_args* args, void* stream);
 
 /* The same step for `count` chunks at once (multi-tensor apply): one
  * persistent TMA launch covers up to 96 chunks (their tiles concatenated),
  * so a step over many small blocks pays one ramp-up / drain / tail instead
  * of one per chunk (chunks of >= 33.5M elements, where that overhead is
- * under 2%, keep their own launch). All entries must share hp, dtypes, param_out presence
- * and the statistics outputs (grad_sq_sum, accumulate_sq, workspace,
- * nonfinite_flag); grad_sq_sum receives the sum over all chunks. Results
+ * under 2%, keep their own launch). Entries may differ in hp (runs of equal
+ * hyper-parameters share a launch: DeepSpeed's counter gives chunk 0 of a
+ * step its own beta^t) but must share dtypes, param_out presence, the
+ * device-side controls and the statistics outputs (grad_sq_sum,
+ * accumulate_sq, workspace, nonfinite_flag); grad_sq_sum receives the sum
+ * over all chunks. Results
  * per element are identical to count fy_adamw_chunk calls (the grad sum of
  * squares up to summation order). Chunks must not overlap. */
 fy_status fy_adamw_chunks(const fy_adamw_args* list, uint32_t count, void* stream);
@@ -148,28 +179,22 @@ fy_status fy_grad_stats(const void* grad, int grad_dtype, uint64_t n, float grad
 fy_status fy_clip_coef(const double* grad_sq_sum, const int* nonfinite, float max_norm,
                        float* scale_out, int* skip_out, void* stream);
 
-/* Tuning of the fused kernel (diagnostics / sweeps), process-wide.
+/* Kernel selection of the fused step (every choice computes the same bits),
+ * process-wide.
  * path 0: LSU kernel, `unroll` quads (4 elements) per thread per grid-stride
- *         iteration in {1,2,4,8}, `ctas_per_sm` resident CTAs (0 = occupancy);
- * path 1: TMA bulk-copy kernel (cp.async.bulk + mbarrier), `unroll` = stages
- *         in {2,3,4,6}, third argument = consumer warps per CTA (4 or 8;
- *         0 = 8; 6 stages only with 8). Default: path 1, 3 stages, 8 warps
- *         (measured best, profiles/). */
+ *         iteration in {1,2,4,8} (0 = 4), `ctas_per_sm` resident CTAs
+ *         (0 = occupancy);
+ * path 1: TMA bulk-copy kernel (cp.async.bulk + mbarrier, one CTA of 8 or
+ *         16 consumer warps + 1 DMA warp per SM), `unroll` = pipeline stages
+ *         in {3,4,6} (fp32 grads: 3 or 6; 0 = auto: 3 on the whole GPU, 4
+ *         under an SM budget), third argument = consumer warps {8,16}
+ *         (0 = auto: 8 on the whole GPU, 16 under an SM budget).
+ * Default: path 1, auto (measured best, profiles/). */
 fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm);
-/* Path 1 sweep variants for bf16 grads -> bf16 params with 8 consumer warps
- * and 2/3/4 stages: `tile` elements per stage (1024, 2048 = default, 4096);
- * `split` = 1 gives the loads and the stores a DMA warp each. `probe`
- * (3 stages x 2048 only): 1 = L2 evict_first cache hints on the bulk
- * copies; 2 = the same traffic with the arithmetic skipped (states written
- * back unchanged: a speed-of-light measurement, not an optimizer step);
- * 3 = both; 4 = the DMA thread computing tile addresses before (not after)
- * waiting for each stage (measured slower); 5 / 6 = refilling the previous
- * tile's stage instead of the one just stored (3 / 4 stages). 0 = off
- * (default). */
-fy_status fy_adamw_tune_bulk(int tile, int split, int probe);
 /* SM budget of the fused step (TMA path), process-wide: launches use at most
  * max_ctas CTAs — one per SM — leaving the other SMs to a backward running
- * concurrently on another stream (0 = every SM, the default). */
+ * concurrently on another stream (0 = every SM, the default). Budgeted
+ * launches run the deeper pipeline (more bytes in flight per SM). */
 fy_status fy_adamw_sm_budget(int max_ctas);
 
 /* Number of SMs and the launch geometry the kernels use on `device`
@@ -182,6 +207,110 @@ fy_status fy_device_info(int device, int* sm_count, int* ctas_per_sm, int* threa
  * the last; returns [offset, count) of `rank`. Pure host arithmetic. */
 fy_status fy_shard_range(uint64_t n, uint32_t world, uint32_t rank, uint32_t align,
                          uint64_t* offset, uint64_t* count);
+
+/* ------------------------------------------------------------------ */
+/* Sharded optimizer step across the GPUs of one node (the
+ * reference's single-GPU optimizer group block, proj/src/task_graph.cpp:
+ * 453-503, with every block split by parameter slice). One fy_shard per GPU
+ * (one process per GPU, or one per device in a single process). Rank r owns
+ * slice r (fy_shard_range, 8-element aligned) of every chunk: the caller
+ * hands it that slice's fp32 [master|m|v] (device memory for
+ * FY_TIER_DEVICE; pinned host memory, ideally fy_host_alloc'd NUMA-local,
+ * for FY_TIER_HOST, streamed through a chunk pipeline) and the slice's
+ * gradients (device). A step updates every owned slice with the fused kernel
+ * and all-gathers the updated 16-bit params, so that every rank ends the
+ * step holding every chunk's full params in the shard's ARENA (device memory
+ * owned by the shard; fy_shard_slice_info gives each chunk's pointer).
+ *
+ * Gather (world > 1):
+ *   FY_GATHER_NCCL  ncclAllGather, in place, per chunk on a comm stream, as
+ *                   soon as the chunk's slice is updated (overlaps the next
+ *                   chunks). Needs nccl_id (fy_nccl_unique_id on rank 0,
+ *                   broadcast out of band).
+ *   FY_GATHER_PEER  no collective: the update kernel's epilogue stores every
+ *                   param into every peer's arena through NVLink (resident
+ *                   tier; the streamed tier pushes each slice with the copy
+ *                   engines), ordered by device-side barriers at the start
+ *                   and end of the step. The peers' arenas come from
+ *                   fy_shard_ipc_handle + fy_shard_connect (processes),
+ *                   fy_shard_connect_ptrs (one process), or — when nccl_id
+ *                   is given — an NCCL all-gather of the handles at create.
+ * The PEER barriers need every rank's stream to make progress while another
+ * rank's barrier spins: one process per GPU always has that; a process that
+ * drives several shards on ONE device must keep its streams (3 per shard)
+ * within CUDA_DEVICE_MAX_CONNECTIONS (default 8; streams beyond it share
+ * hardware queues and serialise). A barrier that waits > 120 s gives up and
+ * fy_shard_wait reports FY_ERR_DEVICE instead of hanging the GPU.
+ * want_grad_norm: the GLOBAL sum of squares over all ranks (one 8-byte
+ * all-reduce, or the exit barrier's exchange summed in rank order).
+ * Step counter: one DeepSpeed IncrementStep per chunk (fy_adam_counter
+ * semantics) unless no_step_counter or hp->beta_t_given. */
+enum { FY_GATHER_NONE = 0, FY_GATHER_NCCL = 1, FY_GATHER_PEER = 2 };
+enum { FY_TIER_DEVICE = 0, FY_TIER_HOST = 1 };
+#define FY_NCCL_ID_BYTES 128
+
+fy_status fy_nccl_unique_id(void* id_out);
+
+typedef struct fy_shard fy_shard;
+typedef struct fy_shard_config {
+    int device;
+    uint32_t world, rank;
+    int gather;                  /* FY_GATHER_*; world 1: none                 */
+    const void* nccl_id;         /* FY_NCCL_ID_BYTES or NULL                   */
+    int tier;                    /* FY_TIER_DEVICE | FY_TIER_HOST              */
+    uint32_t chunk_count;
+    const uint64_t* chunk_elems; /* full chunk sizes, identical on every rank  */
+    int grad_dtype;
+    int param_dtype;
+    uint32_t slots;              /* FY_TIER_HOST: staging slots (0 = 3)        */
+    uint64_t piece_elems;        /* FY_TIER_HOST: max elements per pipeline
+                                    unit (0 = a whole slice)                   */
+    int params_to_host;          /* also D2H each updated slice to io.h_param  */
+    int no_step_counter;
+} fy_shard_config;
+
+typedef struct fy_shard_slice {
+    uint64_t offset, count;      /* this rank's slice of the chunk             */
+    uint64_t stride;             /* padded slice length of every rank          */
+    void* params;                /* device: the chunk's full params (arena)    */
+} fy_shard_slice;
+
+typedef struct fy_shard_io {     /* one per chunk: this rank's buffers         */
+    void* states;                /* [master|m|v] of the slice, 12*count bytes  */
+    const void* grad;            /* device [count] gradients of the slice      */
+    void* h_param;               /* pinned host [count] (params_to_host)       */
+    void* grad_ready;            /* optional cudaEvent_t                       */
+} fy_shard_io;
+
+typedef struct fy_shard_stats {
+    double step_ms;              /* last step, device time (events)            */
+    uint64_t gather_bytes;       /* param bytes this rank sent to peers        */
+    uint64_t h2d_bytes, d2h_bytes;
+    uint32_t world, rank;
+    int gather;                  /* effective FY_GATHER_*                      */
+    int stages;                  /* TMA pipeline stages of the update kernel   */
+    int consumer_warps;          /* TMA consumer warps per CTA                 */
+} fy_shard_stats;
+
+fy_status fy_shard_create(const fy_shard_config* cfg, fy_shard** out);
+void fy_shard_destroy(fy_shard* s);
+fy_status fy_shard_slice_info(const fy_shard* s, uint32_t chunk, fy_shard_slice* out);
+/* The arena: device base pointer and size (header + every chunk's params). */
+fy_status fy_shard_arena(const fy_shard* s, void** base, uint64_t* bytes);
+fy_status fy_shard_ipc_handle(const fy_shard* s, void* handle_out);
+fy_status fy_shard_connect(fy_shard* s, const void* handles);
+fy_status fy_shard_connect_ptrs(fy_shard* s, void* const* arenas);
+/* Enqueues one optimizer step after the work already on `stream` and makes
+ * `stream` wait for its completion (gather included); returns without
+ * blocking. fy_shard_wait blocks until it is done. */
+fy_status fy_shard_step(fy_shard* s, const fy_shard_io* io, const fy_adam_hparams* hp,
+                        int want_grad_norm, void* stream);
+fy_status fy_shard_wait(fy_shard* s, double* grad_sq_sum, int* nonfinite);
+fy_status fy_shard_get_stats(const fy_shard* s, fy_shard_stats* out);
+/* Device time of each chunk's update kernel(s) in the last waited step, ms
+ * (events around the launches on the shard's update stream; streamed tier:
+ * the sum over the chunk's pipeline pieces). */
+fy_status fy_shard_update_ms(const fy_shard* s, double* chunk_ms, uint32_t count);
 
 /* ------------------------------------------------------------------ */
 /* Chunk pipeline: streamed (out-of-core) optimizer step.
@@ -212,6 +341,11 @@ typedef struct fy_pipeline_config {
                                    [master|m|v]; no state copies (the
                                    device-resident tier; grads/params may
                                    still cross the host link) */
+    int no_step_counter;        /* 0 (default): the pipeline is the optimizer
+                                   object and keeps DeepSpeed's step counter
+                                   (fy_adam_counter semantics, one increment
+                                   per chunk update) unless hp->beta_t_given;
+                                   1: every chunk uses hp as given */
 } fy_pipeline_config;
 
 typedef struct fy_chunk {

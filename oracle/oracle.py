@@ -31,6 +31,11 @@ class Scalars(C.Structure):
         "bias_correction2", "step_size", "w_decay", "eps", "weight_decay")] + [("adamw_mode", C.c_int)]
 
 
+class Counter(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("beta1_t", C.c_float), ("beta2_t", C.c_float)]
+
+
 def _load():
     if not _SO.exists():
         raise ImportError(f"{_SO} missing; run `make -C oracle`")
@@ -39,6 +44,13 @@ def _load():
                                                            C.POINTER(Scalars)]
     lib.oracle_adamw_scalars.restype = None
     vp = C.c_void_p
+    lib.oracle_adamw_scalars_bt.argtypes = [C.c_float] * 7 + [C.c_int, C.c_int, C.POINTER(Scalars)]
+    lib.oracle_adamw_scalars_bt.restype = None
+    lib.oracle_counter_init.argtypes = [C.POINTER(Counter), C.c_float, C.c_float]
+    lib.oracle_counter_init.restype = None
+    lib.oracle_counter_increment.argtypes = [C.POINTER(Counter), C.c_uint64, C.c_float, C.c_float,
+                                             C.POINTER(C.c_float), C.POINTER(C.c_float)]
+    lib.oracle_counter_increment.restype = None
     lib.oracle_adamw_step.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, C.c_uint64,
                                       C.POINTER(Scalars), C.c_float, C.POINTER(C.c_double),
                                       C.POINTER(C.c_int)]
@@ -68,6 +80,29 @@ def scalars(lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, step=10,
     LIB.oracle_adamw_scalars(lr, beta1, beta2, eps, weight_decay, step, int(adamw_mode),
                              int(bias_correction), C.byref(s))
     return s
+
+
+def scalars_bt(b1t: float, b2t: float, lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8,
+               weight_decay=0.1, adamw_mode=True, bias_correction=True) -> Scalars:
+    """update_state with explicit float beta1^t / beta2^t (a StepCounter's)."""
+    s = Scalars()
+    LIB.oracle_adamw_scalars_bt(lr, beta1, beta2, eps, weight_decay, b1t, b2t, int(adamw_mode),
+                                int(bias_correction), C.byref(s))
+    return s
+
+
+class StepCounter:
+    """DeepSpeed 0.9.3 Adam_Optimizer IncrementStep (oracle_counter_increment):
+    call next() once per adam_update, i.e. once per chunk."""
+
+    def __init__(self, beta1: float = 0.9, beta2: float = 0.95):
+        self.c = Counter()
+        LIB.oracle_counter_init(C.byref(self.c), beta1, beta2)
+
+    def next(self, step: int, beta1: float = 0.9, beta2: float = 0.95):
+        b1t, b2t = C.c_float(), C.c_float()
+        LIB.oracle_counter_increment(C.byref(self.c), step, beta1, beta2, C.byref(b1t), C.byref(b2t))
+        return b1t.value, b2t.value
 
 
 def _p(a):

@@ -31,8 +31,14 @@ class AdamHparams(C.Structure):
     _fields_ = [
         ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
         ("weight_decay", C.c_float), ("step", C.c_uint64), ("adamw_mode", C.c_int),
-        ("bias_correction", C.c_int), ("grad_scale", C.c_float),
+        ("bias_correction", C.c_int), ("grad_scale", C.c_float), ("beta_t_given", C.c_int),
+        ("beta1_t", C.c_float), ("beta2_t", C.c_float),
     ]
+
+
+class AdamCounter(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("beta1_t", C.c_float), ("beta2_t", C.c_float), ("constructed", C.c_int)]
 
 
 class AdamwArgs(C.Structure):
@@ -50,7 +56,7 @@ class PipelineConfig(C.Structure):
         ("device", C.c_int), ("max_chunk_elems", C.c_uint64), ("slots", C.c_uint32),
         ("grad_dtype", C.c_int), ("param_dtype", C.c_int), ("grads_on_host", C.c_int),
         ("params_to_host", C.c_int), ("keep_params_on_device", C.c_int),
-        ("states_on_device", C.c_int),
+        ("states_on_device", C.c_int), ("no_step_counter", C.c_int),
     ]
 
 
@@ -69,6 +75,38 @@ class SwapConfig(C.Structure):
     ]
 
 
+FY_GATHER_NONE, FY_GATHER_NCCL, FY_GATHER_PEER = 0, 1, 2
+FY_TIER_DEVICE, FY_TIER_HOST = 0, 1
+FY_NCCL_ID_BYTES = 128
+FY_IPC_HANDLE_BYTES = 64
+
+
+class ShardConfig(C.Structure):
+    _fields_ = [
+        ("device", C.c_int), ("world", C.c_uint32), ("rank", C.c_uint32), ("gather", C.c_int),
+        ("nccl_id", C.c_void_p), ("tier", C.c_int), ("chunk_count", C.c_uint32),
+        ("chunk_elems", C.POINTER(C.c_uint64)), ("grad_dtype", C.c_int), ("param_dtype", C.c_int),
+        ("slots", C.c_uint32), ("piece_elems", C.c_uint64), ("params_to_host", C.c_int),
+        ("no_step_counter", C.c_int),
+    ]
+
+
+class ShardSlice(C.Structure):
+    _fields_ = [("offset", C.c_uint64), ("count", C.c_uint64), ("stride", C.c_uint64),
+                ("params", C.c_void_p)]
+
+
+class ShardIo(C.Structure):
+    _fields_ = [("states", C.c_void_p), ("grad", C.c_void_p), ("h_param", C.c_void_p),
+                ("grad_ready", C.c_void_p)]
+
+
+class ShardStats(C.Structure):
+    _fields_ = [("step_ms", C.c_double), ("gather_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("world", C.c_uint32), ("rank", C.c_uint32),
+                ("gather", C.c_int), ("stages", C.c_int), ("consumer_warps", C.c_int)]
+
+
 FY_SWAP_CPU, FY_SWAP_SSD = 0, 1
 FY_CHUNK_STATES_ON_DEVICE = 1
 
@@ -81,12 +119,12 @@ class ChunkTiming(C.Structure):
     ]
 
 
-def _load() -> C.CDLL:
-    if not LIB_PATH.exists():
+def _load(path: Path = LIB_PATH) -> C.CDLL:
+    if not path.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
             " (or `make`). There is no fallback implementation.")
-    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
+    lib = C.CDLL(str(path), mode=os.RTLD_NOW | os.RTLD_LOCAL)
     st = C.c_int
     sig = {
         "fy_version": (C.c_char_p, []),
@@ -98,7 +136,21 @@ def _load() -> C.CDLL:
         "fy_grad_stats": (st, [C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_void_p, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p]),
         "fy_adamw_tune": (st, [C.c_int, C.c_int, C.c_int]),
-        "fy_adamw_tune_bulk": (st, [C.c_int, C.c_int, C.c_int]),
+        "fy_adam_counter_init": (st, [C.POINTER(AdamCounter), C.c_float, C.c_float]),
+        "fy_adam_counter_next": (st, [C.POINTER(AdamCounter), C.POINTER(AdamHparams)]),
+        "fy_nccl_unique_id": (st, [C.c_void_p]),
+        "fy_shard_create": (st, [C.POINTER(ShardConfig), C.POINTER(C.c_void_p)]),
+        "fy_shard_destroy": (None, [C.c_void_p]),
+        "fy_shard_slice_info": (st, [C.c_void_p, C.c_uint32, C.POINTER(ShardSlice)]),
+        "fy_shard_ipc_handle": (st, [C.c_void_p, C.c_void_p]),
+        "fy_shard_arena": (st, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+        "fy_shard_connect": (st, [C.c_void_p, C.c_void_p]),
+        "fy_shard_connect_ptrs": (st, [C.c_void_p, C.POINTER(C.c_void_p)]),
+        "fy_shard_step": (st, [C.c_void_p, C.POINTER(ShardIo), C.POINTER(AdamHparams), C.c_int,
+                               C.c_void_p]),
+        "fy_shard_wait": (st, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
+        "fy_shard_get_stats": (st, [C.c_void_p, C.POINTER(ShardStats)]),
+        "fy_shard_update_ms": (st, [C.c_void_p, C.POINTER(C.c_double), C.c_uint32]),
         "fy_adamw_sm_budget": (st, [C.c_int]),
         "fy_adamw_chunks": (st, [C.POINTER(AdamwArgs), C.c_uint32, C.c_void_p]),
         "fy_clip_coef": (st, [C.c_void_p, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -133,6 +185,8 @@ def _load() -> C.CDLL:
         "fy_device_numa_node": (st, [C.c_int, C.POINTER(C.c_int)]),
         "fy_host_numa_node": (st, [C.c_void_p, C.POINTER(C.c_int)]),
     }
+    if path != LIB_PATH:  # the sweep build (build/sweep) adds the variant selector
+        sig["fy_adamw_tune_bulk"] = (st, [C.c_int, C.c_int, C.c_int])
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
         fn.restype = res
@@ -141,6 +195,14 @@ def _load() -> C.CDLL:
 
 
 LIB = _load()
+
+SWEEP_LIB_PATH = LIB_DIR.parent.parent / "build" / "sweep" / "liboffsim_sweep.so"
+
+
+def load_sweep_lib() -> C.CDLL:
+    """The sweep-only build (make sweep): same ABI plus fy_adamw_tune_bulk's
+    experimental TMA variants. Bench / test tooling only; never the product."""
+    return _load(SWEEP_LIB_PATH)
 
 
 def check(status: int) -> None:

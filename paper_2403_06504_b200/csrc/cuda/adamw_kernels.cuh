@@ -24,9 +24,40 @@ struct AdamScalars {
     const int* skip_dev;    // *skip_dev != 0: the launch writes nothing
 };
 
+// beta^t = float(pow(double(beta), step)) (DeepSpeed's value after a step
+// jump or on a fresh optimizer) ...
 AdamScalars make_scalars(float lr, float beta1, float beta2, float eps, float weight_decay,
                          std::uint64_t step, int adamw_mode, int bias_correction,
                          float grad_scale);
+// ... or given explicitly (b1t / b2t from a StepCounter).
+AdamScalars make_scalars_bt(float lr, float beta1, float beta2, float eps, float weight_decay,
+                            float b1t, float b2t, int adamw_mode, int bias_correction,
+                            float grad_scale);
+// Same per-element arithmetic (device-side controls included)?
+bool same_scalars(const AdamScalars& a, const AdamScalars& b);
+
+// DeepSpeed 0.9.3 Adam_Optimizer step bookkeeping (csrc/includes/cpu_adam.h
+// IncrementStep, called once per adam_update, i.e. once per parameter
+// chunk): while the betas are unchanged and the step number advances by one
+// per call, beta^t is a float running product (beta_t *= beta); any other
+// step number re-evaluates float(pow(double(beta), step)). With K chunks per
+// optimizer step, chunk 0 of step t takes the running product
+// fl(beta^(t-1) * beta) and chunks 1..K-1 (same step number, so the counter
+// "jumps") take pow. A fresh optimizer has step 0 and beta^0 = 1.
+struct StepCounter {
+    std::uint64_t step = 0;
+    float beta1 = 0.0f, beta2 = 0.0f;
+    float beta1_t = 1.0f, beta2_t = 1.0f;
+    bool constructed = false;  // betas of the constructor (first call's when lazily built)
+    void construct(float b1, float b2) {
+        beta1 = b1;
+        beta2 = b2;
+        step = 0;
+        beta1_t = beta2_t = 1.0f;
+        constructed = true;
+    }
+    void increment(std::uint64_t t, float b1, float b2);
+};
 
 // Fused all-gather epilogue: the updated 16-bit params of this launch are
 // also stored at ptr[r] (r < count), each pointing where this rank's slice
@@ -86,19 +117,26 @@ struct Geometry {
 };
 Geometry geometry(int device);
 
-// Tuning knobs (diagnostics / sweeps): path 0 = LSU vector kernel with
-// `unroll` quads per thread (1, 2, 4, 8) and `ctas_per_sm` resident CTAs
-// (0 = occupancy limit); path 1 = TMA bulk kernel with `unroll` pipeline
-// stages (3 or 6).
+// Kernel selection (fy_adamw_tune): path 0 = LSU vector kernel with
+// `unroll` quads per thread (1, 2, 4, 8; 0 = 4) and `ctas_per_sm` resident
+// CTAs (0 = occupancy limit); path 1 = TMA bulk kernel with `unroll`
+// pipeline stages (3, 4, 6; 0 = auto) and `ctas_per_sm` consumer warps (8,
+// 16; 0 = auto: 8 on the whole GPU, 16 under an SM budget).
 void set_tuning(int path, int unroll, int ctas_per_sm);
-// TMA path sweep variants (bf16 -> bf16, 8 consumer warps): elements per
-// stage (1024 | 2048 | 4096) and separate load / store DMA warps; probe
-// (3 stages x 2048): 1 = L2 evict_first hints, 2 = no arithmetic (the
-// access pattern's speed of light; NOT an optimizer), 3 = both.
-void set_bulk_variant(int tile, int split, int probe);
 // SM budget of the TMA path: at most max_ctas CTAs (one per SM; 0 = all SMs)
 // so a concurrent backward keeps the remaining SMs.
 void set_max_ctas(int max_ctas);
+// Stages / consumer warps the TMA path runs on a device with `sms` SMs under
+// the current budget / tuning.
+int tma_stages(int sms);
+int tma_consumer_warps(int sms);
+#ifdef FY_SWEEP_VARIANTS
+// Sweep build only (build/sweep): TMA variants for bf16 -> bf16: elements
+// per stage (1024 | 2048 | 4096), separate load / store DMA warps; probe
+// (3 stages x 2048): 1 = L2 evict_first hints, 2 = no arithmetic (the access
+// pattern's speed of light; NOT an optimizer), 3 = both, 4-6 DMA orders.
+void set_bulk_variant(int tile, int split, int probe);
+#endif
 
 // NUMA-local pinned host memory (host_mem.cu). device_numa_node: the GPU's
 // node from PCI sysfs (-1 unknown). host_alloc: page-locked, portable,

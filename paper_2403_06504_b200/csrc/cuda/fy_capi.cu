@@ -6,6 +6,7 @@
 
 #include "adamw_kernels.cuh"
 #include "pipeline.cuh"
+#include "shard.cuh"
 #include "swap.cuh"
 
 #include <cuda_runtime.h>
@@ -100,8 +101,6 @@ fy_status fy_adamw_chunks(const fy_adamw_args* list, uint32_t count, void* strea
             if (a->grad_dtype != f->grad_dtype || (a->param_out != nullptr) != (f->param_out != nullptr) ||
                 (a->param_out && a->param_dtype != f->param_dtype))
                 return fail(FY_ERR_CONFIG, at + "dtypes / param_out presence differ from chunk 0");
-            if (std::memcmp(&a->hp, &f->hp, sizeof a->hp) != 0)
-                return fail(FY_ERR_CONFIG, at + "hyper-parameters differ from chunk 0");
             if (a->grad_sq_sum != f->grad_sq_sum || a->workspace != f->workspace ||
                 a->nonfinite_flag != f->nonfinite_flag || a->accumulate_sq != f->accumulate_sq)
                 return fail(FY_ERR_CONFIG, at + "statistics outputs differ from chunk 0");
@@ -115,8 +114,7 @@ fy_status fy_adamw_chunks(const fy_adamw_args* list, uint32_t count, void* strea
             l.param = a->param_out;
             l.param_dtype = a->param_dtype;
             l.n = a->n;
-            l.s = fy::make_scalars(a->hp.lr, a->hp.beta1, a->hp.beta2, a->hp.eps, a->hp.weight_decay,
-                                   a->hp.step, a->hp.adamw_mode, a->hp.bias_correction, a->hp.grad_scale);
+            l.s = fy::scalars_of(a->hp);
             l.grad_sq_sum = a->grad_sq_sum;
             l.accumulate_sq = a->accumulate_sq;
             l.workspace = a->workspace;
@@ -160,9 +158,7 @@ fy_status fy_adamw_chunk_impl(const fy_adamw_args* a, void* stream, const fy::Pe
     l.param = a->param_out;
     l.param_dtype = a->param_dtype;
     l.n = a->n;
-    l.s = fy::make_scalars(a->hp.lr, a->hp.beta1, a->hp.beta2, a->hp.eps, a->hp.weight_decay,
-                           a->hp.step, a->hp.adamw_mode, a->hp.bias_correction,
-                           a->hp.grad_scale);
+    l.s = fy::scalars_of(a->hp);
     l.grad_sq_sum = a->grad_sq_sum;
     l.accumulate_sq = a->accumulate_sq;
     l.workspace = a->workspace;
@@ -280,6 +276,101 @@ fy_status fy_pipeline_timings(const fy_pipeline* p, fy_chunk_timing* out, uint32
     if (!p || (!out && count > 0)) return fail(FY_ERR_CONFIG, "null argument");
     return guard([&] {
         p->impl.timings(out, count, step_ns);
+        return FY_OK;
+    });
+}
+
+struct fy_shard {
+    explicit fy_shard(const fy_shard_config& c) : impl(c) {}
+    fy::ShardGroup impl;
+};
+
+fy_status fy_nccl_unique_id(void* id_out) {
+    if (!id_out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        fy::nccl_unique_id(id_out);
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_create(const fy_shard_config* cfg, fy_shard** out) {
+    if (!cfg || !out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        *out = new fy_shard(*cfg);
+        return FY_OK;
+    });
+}
+
+void fy_shard_destroy(fy_shard* s) { delete s; }
+
+fy_status fy_shard_slice_info(const fy_shard* s, uint32_t chunk, fy_shard_slice* out) {
+    if (!s || !out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.slice_info(chunk, out);
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_arena(const fy_shard* s, void** base, uint64_t* bytes) {
+    if (!s || !base || !bytes) return fail(FY_ERR_CONFIG, "null argument");
+    *base = s->impl.arena();
+    *bytes = s->impl.arena_bytes();
+    return FY_OK;
+}
+
+fy_status fy_shard_ipc_handle(const fy_shard* s, void* handle_out) {
+    if (!s || !handle_out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.ipc_handle(handle_out);
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_connect(fy_shard* s, const void* handles) {
+    if (!s || !handles) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.connect_handles(handles);
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_connect_ptrs(fy_shard* s, void* const* arenas) {
+    if (!s || !arenas) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.connect_ptrs(arenas);
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_step(fy_shard* s, const fy_shard_io* io, const fy_adam_hparams* hp, int want_grad_norm,
+                        void* stream) {
+    if (!s || !io || !hp) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.step(io, *hp, want_grad_norm != 0, static_cast<cudaStream_t>(stream));
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_wait(fy_shard* s, double* grad_sq_sum, int* nonfinite) {
+    if (!s) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.wait(grad_sq_sum, nonfinite);
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_get_stats(const fy_shard* s, fy_shard_stats* out) {
+    if (!s || !out) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.stats(out);
+        return FY_OK;
+    });
+}
+
+fy_status fy_shard_update_ms(const fy_shard* s, double* chunk_ms, uint32_t count) {
+    if (!s || (!chunk_ms && count > 0)) return fail(FY_ERR_CONFIG, "null argument");
+    return guard([&] {
+        s->impl.update_ms(chunk_ms, count);
         return FY_OK;
     });
 }
@@ -444,6 +535,30 @@ extern "C" fy_status fy_adamw_sm_budget(int max_ctas) {
     return FY_OK;
 }
 
+extern "C" fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm) {
+    if (path != 0 && path != 1) return fail(FY_ERR_CONFIG, "path must be 0 (LSU) or 1 (TMA bulk)");
+    if (path == 0 && unroll != 0 && unroll != 1 && unroll != 2 && unroll != 4 && unroll != 8)
+        return fail(FY_ERR_CONFIG, "unroll must be 0, 1, 2, 4 or 8");
+    if (ctas_per_sm < 0 || ctas_per_sm > 32) return fail(FY_ERR_CONFIG, "ctas_per_sm out of range");
+#ifdef FY_SWEEP_VARIANTS
+    // sweep build: 2 stages and 4 consumer warps ("narrow") are selectable too
+    if (path == 1 && unroll != 0 && unroll != 2 && unroll != 3 && unroll != 4 && unroll != 6)
+        return fail(FY_ERR_CONFIG, "stages must be 0 (auto), 2, 3, 4 or 6");
+    if (path == 1 && ctas_per_sm != 0 && ctas_per_sm != 4 && ctas_per_sm != 8 && ctas_per_sm != 16)
+        return fail(FY_ERR_CONFIG, "path 1: third argument is the consumer warp count (4, 8 or 16)");
+#else
+    if (path == 1 && unroll != 0 && unroll != 3 && unroll != 4 && unroll != 6)
+        return fail(FY_ERR_CONFIG, "stages must be 0 (auto), 3, 4 or 6");
+    if (path == 1 && ctas_per_sm != 0 && ctas_per_sm != 8 && ctas_per_sm != 16)
+        return fail(FY_ERR_CONFIG, "path 1: third argument is the consumer warp count (0 = auto, 8, 16)");
+#endif
+    fy::set_tuning(path, unroll, ctas_per_sm);
+    return FY_OK;
+}
+
+#ifdef FY_SWEEP_VARIANTS
+// Sweep build only (build/sweep/liboffsim_sweep.so): TMA kernel variants
+// that are not product configurations (see adamw_kernels.cu dispatch_sweep).
 extern "C" fy_status fy_adamw_tune_bulk(int tile, int split, int probe) {
     if (tile != 1024 && tile != 2048 && tile != 4096) return fail(FY_ERR_CONFIG, "tile must be 1024, 2048 or 4096");
     if (split != 0 && split != 1) return fail(FY_ERR_CONFIG, "split must be 0 or 1");
@@ -451,16 +566,24 @@ extern "C" fy_status fy_adamw_tune_bulk(int tile, int split, int probe) {
     fy::set_bulk_variant(tile, split, probe);
     return FY_OK;
 }
+#endif
 
-extern "C" fy_status fy_adamw_tune(int path, int unroll, int ctas_per_sm) {
-    if (path != 0 && path != 1) return fail(FY_ERR_CONFIG, "path must be 0 (LSU) or 1 (TMA bulk)");
-    if (path == 0 && unroll != 1 && unroll != 2 && unroll != 4 && unroll != 8)
-        return fail(FY_ERR_CONFIG, "unroll must be 1, 2, 4 or 8");
-    if (path == 1 && (unroll < 2 || unroll > 6 || unroll == 5))
-        return fail(FY_ERR_CONFIG, "stages must be 2, 3, 4 or 6");
-    if (ctas_per_sm < 0 || ctas_per_sm > 32) return fail(FY_ERR_CONFIG, "ctas_per_sm out of range");
-    if (path == 1 && ctas_per_sm != 0 && ctas_per_sm != 4 && ctas_per_sm != 8)
-        return fail(FY_ERR_CONFIG, "path 1: third argument is the consumer warp count (4 or 8)");
-    fy::set_tuning(path, unroll, ctas_per_sm);
+extern "C" fy_status fy_adam_counter_init(fy_adam_counter* c, float beta1, float beta2) {
+    if (!c) return fail(FY_ERR_CONFIG, "null argument");
+    fy::StepCounter k;
+    k.construct(beta1, beta2);
+    fy::store_counter(k, c);
+    return FY_OK;
+}
+
+extern "C" fy_status fy_adam_counter_next(fy_adam_counter* c, fy_adam_hparams* hp) {
+    if (!c || !hp) return fail(FY_ERR_CONFIG, "null argument");
+    if (hp->step == 0) return fail(FY_ERR_CONFIG, "step must be >= 1");
+    fy::StepCounter k = fy::load_counter(*c);
+    k.increment(hp->step, hp->beta1, hp->beta2);
+    fy::store_counter(k, c);
+    hp->beta_t_given = 1;
+    hp->beta1_t = k.beta1_t;
+    hp->beta2_t = k.beta2_t;
     return FY_OK;
 }

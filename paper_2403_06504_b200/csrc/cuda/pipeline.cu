@@ -34,6 +34,34 @@ void check_cuda(cudaError_t e, const char* what) {
                           cudaGetErrorString(e) + ")");
 }
 
+AdamScalars scalars_of(const fy_adam_hparams& hp) {
+    if (hp.beta_t_given)
+        return make_scalars_bt(hp.lr, hp.beta1, hp.beta2, hp.eps, hp.weight_decay, hp.beta1_t, hp.beta2_t,
+                               hp.adamw_mode, hp.bias_correction, hp.grad_scale);
+    return make_scalars(hp.lr, hp.beta1, hp.beta2, hp.eps, hp.weight_decay, hp.step, hp.adamw_mode,
+                        hp.bias_correction, hp.grad_scale);
+}
+
+StepCounter load_counter(const fy_adam_counter& c) {
+    StepCounter k;
+    k.step = c.step;
+    k.beta1 = c.beta1;
+    k.beta2 = c.beta2;
+    k.beta1_t = c.beta1_t;
+    k.beta2_t = c.beta2_t;
+    k.constructed = c.constructed != 0;
+    return k;
+}
+
+void store_counter(const StepCounter& k, fy_adam_counter* c) {
+    c->step = k.step;
+    c->beta1 = k.beta1;
+    c->beta2 = k.beta2;
+    c->beta1_t = k.beta1_t;
+    c->beta2_t = k.beta2_t;
+    c->constructed = k.constructed ? 1 : 0;
+}
+
 namespace {
 int dtype_bytes(int dt) { return dt == FY_FP32 ? 4 : 2; }
 } // namespace
@@ -169,7 +197,17 @@ void ChunkPipeline::issue_update(std::uint32_t i) {
     a.param = cfg_.keep_params_on_device ? c.d_param : (cfg_.params_to_host ? slot.param : nullptr);
     a.param_dtype = cfg_.param_dtype;
     a.n = c.n;
-    a.s = scalars_;
+    // one DeepSpeed adam_update per chunk: the counter advances per chunk
+    fy_adam_hparams hp = unit_hp_ ? unit_hp_[i] : hp_;
+    if (!cfg_.no_step_counter && !hp.beta_t_given) {
+        counter_.increment(hp.step, hp.beta1, hp.beta2);
+        hp.beta_t_given = 1;
+        hp.beta1_t = counter_.beta1_t;
+        hp.beta2_t = counter_.beta2_t;
+    }
+    a.s = scalars_of(hp);
+    a.s.scale_dev = scale_dev_;  // a skipped update still writes params from master
+    a.s.skip_dev = skip_dev_;
     a.grad_sq_sum = want_norm_ ? d_norm_ : nullptr;
     a.accumulate_sq = 1;
     a.workspace = workspace_;
@@ -207,7 +245,7 @@ void ChunkPipeline::issue_d2h(std::uint32_t i) {
 }
 
 void ChunkPipeline::step(const fy_chunk* chunks, std::uint32_t count, const fy_adam_hparams& hp,
-                         bool want_norm) {
+                         bool want_norm, const fy_adam_hparams* per_chunk_hp, cudaEvent_t start_after) {
     if (pending_) throw ArgError("pipeline: previous step not waited");
     if (count == 0) throw ArgError("pipeline: empty step");
     for (std::uint32_t i = 0; i < count; ++i) {
@@ -225,13 +263,12 @@ void ChunkPipeline::step(const fy_chunk* chunks, std::uint32_t count, const fy_a
     ensure_events(count);
     chunks_ = chunks;
     want_norm_ = want_norm;
-    scalars_ = make_scalars(hp.lr, hp.beta1, hp.beta2, hp.eps, hp.weight_decay, hp.step,
-                            hp.adamw_mode, hp.bias_correction, hp.grad_scale);
-    scalars_.scale_dev = scale_dev_;  // a skipped update still writes params from master
-    scalars_.skip_dev = skip_dev_;
+    hp_ = hp;
+    unit_hp_ = per_chunk_hp;
 
     // Step boundary: the previous step's write-backs own the slots.
     if (have_prev_) check_cuda(cudaStreamWaitEvent(h2d_, step_end_, 0), "wait prev");
+    if (start_after) check_cuda(cudaStreamWaitEvent(h2d_, start_after, 0), "wait start_after");
     check_cuda(cudaEventRecord(step_start_, h2d_), "record");
     check_cuda(cudaStreamWaitEvent(opt_, step_start_, 0), "wait start");
     check_cuda(cudaMemsetAsync(d_norm_, 0, sizeof(double), opt_), "memset");
@@ -249,6 +286,7 @@ void ChunkPipeline::step(const fy_chunk* chunks, std::uint32_t count, const fy_a
                "flag");
     check_cuda(cudaEventRecord(step_end_, d2h_), "record");
     chunks_ = nullptr;
+    unit_hp_ = nullptr;
     pending_ = true;
     have_prev_ = true;
     last_count_ = count;

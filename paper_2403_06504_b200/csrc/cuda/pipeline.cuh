@@ -23,6 +23,12 @@ struct ArgError : std::runtime_error {
 
 void check_cuda(cudaError_t e, const char* what);
 
+// Kernel scalars of one update: beta^t from hp (given) or pow(step).
+AdamScalars scalars_of(const fy_adam_hparams& hp);
+// fy_adam_counter <-> StepCounter
+StepCounter load_counter(const fy_adam_counter& c);
+void store_counter(const StepCounter& k, fy_adam_counter* c);
+
 // Device staging for one chunk in flight: [master | m | v] (12n B), plus a
 // gradient area (host-sourced grads) and a param area (downcast output).
 struct Slot {
@@ -39,8 +45,12 @@ public:
     ChunkPipeline(const ChunkPipeline&) = delete;
     ChunkPipeline& operator=(const ChunkPipeline&) = delete;
 
+    // per_chunk_hp (optional, count entries): each unit's own hyper-parameters
+    // (the sharded step passes one chunk's beta^t to all of its pieces);
+    // start_after (optional): the step's first operations wait on this event.
     void step(const fy_chunk* chunks, std::uint32_t count, const fy_adam_hparams& hp,
-              bool want_norm);
+              bool want_norm, const fy_adam_hparams* per_chunk_hp = nullptr,
+              cudaEvent_t start_after = nullptr);
     void wait(double* grad_sq_sum, int* nonfinite);
     void timings(fy_chunk_timing* out, std::uint32_t count, std::uint64_t* step_ns) const;
     // device-side clip coefficient / overflow-skip flag for the following
@@ -53,6 +63,13 @@ public:
     cudaStream_t h2d_stream() const { return h2d_; }
     cudaStream_t d2h_stream() const { return d2h_; }
     cudaStream_t compute_stream() const { return opt_; }
+    // device-side sum of squares / non-finite flag of the step in flight and
+    // the event recorded when all of its work (copies included) is done
+    double* device_norm() const { return d_norm_; }
+    int* device_nonfinite() const { return d_nonfinite_; }
+    cudaEvent_t step_end_event() const { return step_end_; }
+    // the step's work is complete (host side: marks it waited without a sync)
+    void mark_waited() { pending_ = false; }
 
 private:
     enum Ev { kH2dStart, kH2dEnd, kUpdStart, kUpdEnd, kD2hStart, kD2hEnd, kEvPerChunk };
@@ -86,7 +103,9 @@ private:
     std::uint32_t last_count_ = 0;
     // Current step's inputs (valid during step()).
     const fy_chunk* chunks_ = nullptr;
-    AdamScalars scalars_{};
+    fy_adam_hparams hp_{};
+    const fy_adam_hparams* unit_hp_ = nullptr;
+    StepCounter counter_{};  // DeepSpeed Adam_Optimizer step bookkeeping (unless no_step_counter)
     const float* scale_dev_ = nullptr;
     const int* skip_dev_ = nullptr;
 };

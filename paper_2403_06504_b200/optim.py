@@ -7,13 +7,16 @@ argument meaning and error behaviour are those of ``include/fuyou/fy_adam.h``.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
 import torch
 
-from ._lib import (LIB, AdamHparams, AdamwArgs, Chunk, ChunkTiming, FY_BF16, FY_FP16, FY_FP32,
-                   FY_SWAP_CPU, FY_SWAP_SSD, PipelineConfig, SwapConfig, check)
+from ._lib import (LIB, AdamCounter, AdamHparams, AdamwArgs, Chunk, ChunkTiming, FY_BF16, FY_FP16, FY_FP32,
+                   FY_GATHER_NCCL, FY_GATHER_NONE, FY_GATHER_PEER, FY_IPC_HANDLE_BYTES, FY_NCCL_ID_BYTES,
+                   FY_SWAP_CPU, FY_SWAP_SSD, FY_TIER_DEVICE, FY_TIER_HOST, PipelineConfig, ShardConfig,
+                   ShardIo, ShardSlice, ShardStats, SwapConfig, FyError, check)
 
 _DT = {torch.bfloat16: FY_BF16, torch.float16: FY_FP16, torch.float32: FY_FP32}
 
@@ -34,11 +37,31 @@ class Hparams:
     adamw_mode: bool = True
     bias_correction: bool = True
     grad_scale: float = 1.0
+    # beta^t given (DeepSpeed running product, from a StepCounter) or None:
+    # float(pow(double(beta), step))
+    beta_t: Optional[tuple] = None
 
     def c(self) -> AdamHparams:
+        bt = self.beta_t
         return AdamHparams(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay,
                            self.step, int(self.adamw_mode), int(self.bias_correction),
-                           self.grad_scale)
+                           self.grad_scale, int(bt is not None), bt[0] if bt else 0.0,
+                           bt[1] if bt else 0.0)
+
+
+class StepCounter:
+    """fy_adam_counter: DeepSpeed's Adam_Optimizer step bookkeeping. next(hp)
+    returns a copy of hp with beta_t set (one call per chunk update)."""
+
+    def __init__(self, beta1: Optional[float] = None, beta2: Optional[float] = None):
+        self.c = AdamCounter()
+        if beta1 is not None:
+            check(LIB.fy_adam_counter_init(C.byref(self.c), beta1, beta2))
+
+    def next(self, hp: "Hparams") -> "Hparams":
+        h = hp.c()
+        check(LIB.fy_adam_counter_next(C.byref(self.c), C.byref(h)))
+        return dataclasses.replace(hp, beta_t=(h.beta1_t, h.beta2_t))
 
 
 def workspace_floats() -> int:
@@ -55,10 +78,11 @@ def adamw_chunk(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.T
                 workspace: Optional[torch.Tensor] = None, nonfinite: Optional[torch.Tensor] = None,
                 stream: Optional[torch.cuda.Stream] = None, n: Optional[int] = None,
                 grad_scale_dev: Optional[torch.Tensor] = None,
-                skip_if_set: Optional[torch.Tensor] = None) -> None:
+                skip_if_set: Optional[torch.Tensor] = None, lib=None) -> None:
     """Enqueue the fused step on ``stream`` (default: torch's current stream).
     grad_scale_dev (device float32[1]) / skip_if_set (device int32[1]):
-    the device-side controls written by clip_coef()."""
+    the device-side controls written by clip_coef(). lib: another build of
+    the same ABI (the sweep build in kernel sweeps); default the product."""
     if stream is None:
         stream = torch.cuda.current_stream(master.device)
     a = AdamwArgs()
@@ -75,7 +99,10 @@ def adamw_chunk(master: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.T
     a.nonfinite_flag = _ptr(nonfinite)
     a.grad_scale_dev = _ptr(grad_scale_dev)
     a.skip_if_set = _ptr(skip_if_set)
-    check(LIB.fy_adamw_chunk(C.byref(a), C.c_void_p(stream.cuda_stream)))
+    lib = LIB if lib is None else lib
+    st = lib.fy_adamw_chunk(C.byref(a), C.c_void_p(stream.cuda_stream))
+    if st:
+        raise FyError(st, lib.fy_last_error().decode())
 
 
 def clip_coef(grad_sq_sum: torch.Tensor, nonfinite: Optional[torch.Tensor], max_norm: float,
@@ -171,10 +198,11 @@ class ChunkPipeline:
     def __init__(self, max_chunk_elems: int, slots: int = 3, device: int = 0,
                  grad_dtype: torch.dtype = torch.bfloat16, param_dtype: torch.dtype = torch.bfloat16,
                  grads_on_host: bool = False, params_to_host: bool = True,
-                 keep_params_on_device: bool = False, states_on_device: bool = False):
+                 keep_params_on_device: bool = False, states_on_device: bool = False,
+                 no_step_counter: bool = False):
         cfg = PipelineConfig(device, max_chunk_elems, slots, fy_dtype(grad_dtype),
                              fy_dtype(param_dtype), int(grads_on_host), int(params_to_host),
-                             int(keep_params_on_device), int(states_on_device))
+                             int(keep_params_on_device), int(states_on_device), int(no_step_counter))
         h = C.c_void_p()
         check(LIB.fy_pipeline_create(C.byref(cfg), C.byref(h)))
         self._h = h
@@ -280,6 +308,108 @@ class Swapper:
     def close(self):
         if self._h:
             LIB.fy_swapper_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    """fy_nccl_unique_id: rank 0 creates it, every rank passes the same bytes."""
+    buf = C.create_string_buffer(FY_NCCL_ID_BYTES)
+    check(LIB.fy_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Shard:
+    """Sharded optimizer step across the GPUs of a node (fy_shard_*).
+
+    chunk_elems: every chunk's full size (same on all ranks). gather: "nccl",
+    "peer" or None (world 1). tier: "device" (states in HBM) or "host"
+    (pinned host states streamed through the chunk pipeline)."""
+    GATHER = {None: FY_GATHER_NONE, "none": FY_GATHER_NONE, "nccl": FY_GATHER_NCCL, "peer": FY_GATHER_PEER}
+
+    def __init__(self, chunk_elems: Sequence[int], world: int = 1, rank: int = 0, device: int = 0,
+                 gather: Optional[str] = None, nccl_id: Optional[bytes] = None, tier: str = "device",
+                 grad_dtype: torch.dtype = torch.bfloat16, param_dtype: torch.dtype = torch.bfloat16,
+                 slots: int = 0, piece_elems: int = 0, params_to_host: bool = False,
+                 no_step_counter: bool = False):
+        self.chunk_elems = list(chunk_elems)
+        self._elems = (C.c_uint64 * len(self.chunk_elems))(*self.chunk_elems)
+        self._id = C.create_string_buffer(nccl_id, FY_NCCL_ID_BYTES) if nccl_id is not None else None
+        cfg = ShardConfig(device, world, rank, self.GATHER[gather],
+                          C.cast(self._id, C.c_void_p) if self._id is not None else None,
+                          FY_TIER_HOST if tier == "host" else FY_TIER_DEVICE, len(self.chunk_elems),
+                          self._elems, fy_dtype(grad_dtype), fy_dtype(param_dtype), slots, piece_elems,
+                          int(params_to_host), int(no_step_counter))
+        h = C.c_void_p()
+        check(LIB.fy_shard_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self._io = None
+        self.world, self.rank = world, rank
+
+    def slice(self, c: int) -> dict:
+        s = ShardSlice()
+        check(LIB.fy_shard_slice_info(self._h, c, C.byref(s)))
+        return dict(offset=s.offset, count=s.count, stride=s.stride, params=s.params)
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(FY_IPC_HANDLE_BYTES)
+        check(LIB.fy_shard_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def connect(self, handles: Sequence[bytes]) -> None:
+        blob = b"".join(handles)
+        check(LIB.fy_shard_connect(self._h, C.create_string_buffer(blob, len(blob))))
+
+    def connect_ptrs(self, arenas: Sequence[int]) -> None:
+        arr = (C.c_void_p * len(arenas))(*arenas)
+        check(LIB.fy_shard_connect_ptrs(self._h, arr))
+
+    def arena(self) -> int:
+        """Base of this shard's arena (what peers in the same process pass to
+        connect_ptrs)."""
+        base, size = C.c_void_p(), C.c_uint64()
+        check(LIB.fy_shard_arena(self._h, C.byref(base), C.byref(size)))
+        return base.value
+
+    def step(self, io: Sequence[dict], hp: Hparams, want_grad_norm: bool = False,
+             stream: Optional[torch.cuda.Stream] = None) -> None:
+        """io[c] = dict(states=ptr, grad=ptr[, h_param=ptr, grad_ready=cudaEvent])."""
+        arr = (ShardIo * len(io))()
+        for i, d in enumerate(io):
+            ev = d.get("grad_ready")
+            arr[i] = ShardIo(d.get("states"), d.get("grad"), d.get("h_param"),
+                             ev.cuda_event if ev is not None and hasattr(ev, "cuda_event") else ev)
+        self._io = arr
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        check(LIB.fy_shard_step(self._h, arr, C.byref(hp.c()), int(want_grad_norm),
+                                C.c_void_p(stream.cuda_stream)))
+
+    def wait(self):
+        sq, bad = C.c_double(), C.c_int()
+        check(LIB.fy_shard_wait(self._h, C.byref(sq), C.byref(bad)))
+        self._io = None
+        return sq.value, bad.value
+
+    def update_ms(self) -> list:
+        """Per chunk: device time of its update kernel(s) in the last step."""
+        arr = (C.c_double * len(self.chunk_elems))()
+        check(LIB.fy_shard_update_ms(self._h, arr, len(self.chunk_elems)))
+        return list(arr)
+
+    def stats(self) -> dict:
+        st = ShardStats()
+        check(LIB.fy_shard_get_stats(self._h, C.byref(st)))
+        return {k: getattr(st, k) for k, _ in ShardStats._fields_}
+
+    def close(self):
+        if self._h:
+            LIB.fy_shard_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -13,7 +13,9 @@ import torch
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from paper_2403_06504_b200 import optim as F  # noqa: E402
-from paper_2403_06504_b200._lib import LIB, check  # noqa: E402
+from paper_2403_06504_b200._lib import check, load_sweep_lib  # noqa: E402
+
+LIB = load_sweep_lib()  # the sweep build (make sweep): product + experimental TMA variants
 
 N = 12 * 5120 * 5120
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 6
@@ -42,7 +44,7 @@ for path, unroll, cps, tile, split, probe in configs * 2:  # two passes: run-to-
         def launch(k):
             st = states[k]
             F.adamw_chunk(st[:N], st[N:2 * N], st[2 * N:], grads[k], hp, param_out=grads[k],
-                          grad_sq_sum=sq, workspace=ws, nonfinite=bad)
+                          grad_sq_sum=sq, workspace=ws, nonfinite=bad, lib=LIB)
         for k in range(K):
             launch(k)
         torch.cuda.synchronize()
@@ -60,7 +62,7 @@ for path, unroll, cps, tile, split, probe in configs * 2:  # two passes: run-to-
                             gbs=gbs, frac=gbs / peak))
         print(f"path={path} unroll={unroll} ctas_per_sm={cps} tile={tile} split={split} probe={probe}: {ms:.3f} ms/launch  "
               f"{gbs:.0f} GB/s  {gbs / peak:.3f} of peak", flush=True)
-check(LIB.fy_adamw_tune(1, 3, 0))
+check(LIB.fy_adamw_tune(1, 0, 0))
 check(LIB.fy_adamw_tune_bulk(2048, 0, 0))
 best = max(results, key=lambda r: r["gbs"])
 print("BEST", json.dumps(best))

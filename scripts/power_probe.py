@@ -16,7 +16,9 @@ import torch
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from paper_2403_06504_b200 import optim as F  # noqa: E402
-from paper_2403_06504_b200._lib import LIB, check  # noqa: E402
+from paper_2403_06504_b200._lib import check, load_sweep_lib  # noqa: E402
+
+LIB = load_sweep_lib()  # the sweep build (make sweep): product + experimental TMA variants
 
 N = 12 * 5120 * 5120
 K = 40
@@ -34,7 +36,7 @@ def step():
     for k in range(K):
         st = states[k]
         F.adamw_chunk(st[:N], st[N:2 * N], st[2 * N:], grads[k], hp, param_out=grads[k], grad_sq_sum=sq,
-                      workspace=ws)
+                      workspace=ws, lib=LIB)
 
 
 VARIANTS = {
@@ -85,5 +87,5 @@ for name, tune, bulk, *budget in VARIANTS[sys.argv[1] if len(sys.argv) > 1 else 
     print(json.dumps({"variant": name, "ms_per_step": ms, "gbs": 28 * N * K / (ms * 1e-3) / 1e9,
                       "power_w_median": statistics.median(p for p, _ in tail),
                       "sm_mhz_median": statistics.median(c for _, c in tail), "samples": len(tail)}), flush=True)
-check(LIB.fy_adamw_tune(1, 3, 0))
+check(LIB.fy_adamw_tune(1, 0, 0))
 check(LIB.fy_adamw_tune_bulk(2048, 0, 0))

@@ -90,8 +90,10 @@ def test_argument_validation_without_gpu():
     assert b"param_out" in LIB.fy_last_error()
     assert LIB.fy_adamw_tune(2, 3, 0) == FY_ERR_CONFIG
     assert LIB.fy_adamw_tune(0, 3, 0) == FY_ERR_CONFIG
-    assert LIB.fy_adamw_tune(1, 5, 0) == FY_ERR_CONFIG
-    assert LIB.fy_adamw_tune(1, 3, 2) == FY_ERR_CONFIG
+    assert LIB.fy_adamw_tune(1, 2, 0) == FY_ERR_CONFIG  # 2 stages: sweep build only
+    assert LIB.fy_adamw_tune(1, 8, 0) == FY_ERR_CONFIG
+    assert LIB.fy_adamw_tune(1, 3, 4) == FY_ERR_CONFIG  # 4 consumer warps: sweep build only
+    assert not hasattr(LIB, "fy_adamw_tune_bulk"), "sweep-only variants must not ship in the product"
     h = C.c_void_p()
     cfg = PipelineConfig(0, 1024, 1, 0, 0, 0, 1, 0, 0)
     assert LIB.fy_pipeline_create(C.byref(cfg), C.byref(h)) == FY_ERR_CONFIG

@@ -110,3 +110,60 @@ def test_omp_equals_scalar():
     for x, y in zip(a + [pa], b + [pb]):
         assert np.array_equal(x.view(np.uint32) if x.dtype == np.float32 else x,
                               y.view(np.uint32) if y.dtype == np.float32 else y)
+
+
+TRAJ = Path(__file__).resolve().parent / "golden" / "adamw_trajectory_golden.npz"
+
+
+def trajectory_check(s, c, old, got, gold, grad_bits):
+    """One step of chunk c against torch (fed forward from torch's previous
+    state). Two bars (north star: "rel 1e-6 on params and m/v"):
+      * every element: within 1e-6 of the magnitude of its summands (_bound);
+      * per-element RELATIVE 1e-6 wherever the result is well conditioned
+        (condition number <= 4: the summands do not cancel — for m,
+        (b1|m_old| + (1-b1)|g|) / |m|; for params, (|p_old| + |upd| cond_m)
+        / |p|, since the update inherits m's cancellation); v never cancels,
+        so all of v. The well-conditioned share is asserted too.
+    Returns the covered fractions."""
+    p0, m0, v0 = old
+    p, m, v = got
+    tp, tm, tv = gold
+    gf = (grad_bits.astype(np.uint32) << 16).view(np.float32)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        cond_m = (0.9 * np.abs(m0) + 0.1 * np.abs(gf)) / np.abs(tm)
+        upd = np.abs(tp - p0)
+        cond_p = (np.abs(p0) + upd * np.where(np.isfinite(cond_m), cond_m, 1e30)) / np.abs(tp)
+        rel = lambda x, r: np.abs(x - r) / np.abs(r)
+        assert _close(m, tm, _bound(0.9 * m0, 0.1 * gf)), f"m step {s} chunk {c}"
+        assert _close(v, tv, _bound(0.95 * v0, 0.05 * gf * gf)), f"v step {s} chunk {c}"
+        assert _close(p, tp, _bound(p0, upd) + 4 * RTOL * upd), f"p step {s} chunk {c}"
+        okm, okp = cond_m <= 4, cond_p <= 4
+        assert np.all(rel(m, tm)[okm] <= RTOL), f"m rel step {s} chunk {c}"
+        assert np.all(rel(p, tp)[okp] <= RTOL), f"p rel step {s} chunk {c}"
+        assert np.all(rel(v, tv)[tv != 0] <= RTOL), f"v rel step {s} chunk {c}"
+    return okm.mean(), okp.mean()
+
+
+def oracle_trajectory(counter=True):
+    """The oracle over the fixture: per step, every chunk from torch's
+    previous state, beta^t from DeepSpeed's step counter (one increment per
+    chunk, as DeepSpeedCPUAdam calls adam_update per sub-group)."""
+    g = np.load(TRAJ)
+    sizes, steps = [int(x) for x in g["sizes"]], int(g["steps"])
+    k = O.StepCounter()
+    for s in range(steps):
+        for c, n in enumerate(sizes):
+            if s == 0:
+                old = (g[f"c{c}_master0"], np.zeros(n, np.float32), np.zeros(n, np.float32))
+            else:
+                old = (g[f"c{c}_master{s}"], g[f"c{c}_m{s}"], g[f"c{c}_v{s}"])
+            st = [x.copy() for x in old]
+            sc = O.scalars_bt(*k.next(s + 1)) if counter else O.scalars(step=s + 1)
+            gb = np.ascontiguousarray(g[f"c{c}_grads"][s])
+            O.adamw_step(*st, gb, O.BF16, sc)
+            yield s, c, old, st, (g[f"c{c}_master{s + 1}"], g[f"c{c}_m{s + 1}"], g[f"c{c}_v{s + 1}"]), gb
+
+
+def test_oracle_trajectory_with_step_counter_matches_torch():
+    cov = [trajectory_check(s, c, old, st, gold, gb) for s, c, old, st, gold, gb in oracle_trajectory()]
+    assert np.mean([a for a, _ in cov]) > 0.8 and np.mean([b for _, b in cov]) > 0.99

@@ -46,14 +46,15 @@ def test_pipeline_matches_oracle(cuda_dev, grads_on_host, slots):
     chunks, ref = _make_chunks(sizes, 1, cuda_dev, grads_on_host)
     pipe = F.ChunkPipeline(max(sizes), slots=slots, grads_on_host=grads_on_host)
     sq_total = 0.0
+    counter = O.StepCounter()  # the pipeline keeps DeepSpeed's step counter
     for step in (10, 11):
         hp = F.Hparams(step=step)
         pipe.step(_desc(chunks), hp, want_grad_norm=True)
         sq, bad = pipe.wait()
         assert bad == 0
-        sc = O.scalars(step=step)
         sq_ref = 0.0
         for r in ref:
+            sc = O.scalars_bt(*counter.next(step))
             n = r["grad"].size
             st = r["states"]
             r["param"] = np.zeros(n, np.uint16)
@@ -314,11 +315,12 @@ def test_pipeline_mixed_resident_and_streamed_chunks(cuda_dev):
         desc[k]["h_states"] = dev_states[k].data_ptr()
         desc[k]["flags"] = FY_CHUNK_STATES_ON_DEVICE
     pipe = F.ChunkPipeline(max(sizes), slots=2)
+    counter = O.StepCounter()
     for step in (10, 11):
         pipe.step(desc, F.Hparams(step=step))
         pipe.wait()
-        sc = O.scalars(step=step)
         for k, (c, r) in enumerate(zip(chunks, ref)):
+            sc = O.scalars_bt(*counter.next(step))
             n = r["grad"].size
             st = r["states"]
             mst, mm, vv = st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()
@@ -329,3 +331,78 @@ def test_pipeline_mixed_resident_and_streamed_chunks(cuda_dev):
             assert _bits_equal(got, r["states"]), f"chunk {k} step {step}"
             assert np.array_equal(c["h_param_t"].view(torch.int16).numpy().view(np.uint16), op)
     pipe.close()
+
+
+def _traj():
+    from pathlib import Path
+    g = np.load(Path(__file__).resolve().parent / "golden" / "adamw_trajectory_golden.npz")
+    return g, [int(x) for x in g["sizes"]], int(g["steps"])
+
+
+def test_pipeline_deepspeed_trajectory_bit_exact(cuda_dev):
+    """Six consecutive steps from fresh states over four chunks through the
+    pipeline, which keeps DeepSpeed's step counter (chunk 0 of every step on
+    the running product of beta^t, the others on pow): bit-exact vs the
+    oracle run with the same counter, step by step."""
+    from paper_2403_06504_b200 import optim as F
+    g, sizes, steps = _traj()
+    host, ref = [], []
+    for c, n in enumerate(sizes):
+        st = np.concatenate([g[f"c{c}_master0"], np.zeros(2 * n, np.float32)])
+        host.append(dict(n=n, h_states_t=torch.from_numpy(st.copy()).pin_memory(),
+                         h_param_t=torch.zeros(n, dtype=torch.bfloat16).pin_memory()))
+        ref.append([st[:n].copy(), st[n:2 * n].copy(), st[2 * n:].copy()])
+    pipe = F.ChunkPipeline(max(sizes), slots=2)
+    k = O.StepCounter()
+    for s in range(steps):
+        grads = [torch.from_numpy(np.ascontiguousarray(g[f"c{c}_grads"][s]).view(np.int16)).view(torch.bfloat16)
+                 .to(cuda_dev) for c in range(len(sizes))]
+        desc = [dict(n=h["n"], h_states=h["h_states_t"].data_ptr(), grad=gr.data_ptr(),
+                     h_param=h["h_param_t"].data_ptr()) for h, gr in zip(host, grads)]
+        pipe.step(desc, F.Hparams(step=s + 1))
+        pipe.wait()
+        for c, (h, r) in enumerate(zip(host, ref)):
+            op = np.zeros(h["n"], np.uint16)
+            O.adamw_step(*r, np.ascontiguousarray(g[f"c{c}_grads"][s]), O.BF16, O.scalars_bt(*k.next(s + 1)),
+                         param_out=op)
+            assert _bits_equal(h["h_states_t"].numpy(), np.concatenate(r)), f"step {s + 1} chunk {c}"
+            assert np.array_equal(h["h_param_t"].view(torch.int16).numpy().view(np.uint16), op)
+    pipe.close()
+
+
+def test_chunks_with_counter_hparams_vs_torch_and_oracle(cuda_dev):
+    """fy_adamw_chunks with per-chunk hyper-parameters from fy_adam_counter
+    (chunk 0 differs from the rest: separate launches inside one call), fed
+    from torch's previous state every step: bit-exact vs the oracle and
+    within the north star's tolerance of torch.optim.AdamW (per-element
+    relative 1e-6 where well conditioned, summand bound everywhere;
+    tests/test_oracle_golden.trajectory_check)."""
+    from paper_2403_06504_b200 import optim as F
+    from test_oracle_golden import oracle_trajectory, trajectory_check
+    g, sizes, steps = _traj()
+    counter = F.StepCounter()
+    by_step = {}
+    for s, c, old, st, gold, gb in oracle_trajectory():
+        by_step.setdefault(s, []).append((c, old, st, gold, gb))
+    for s in range(steps):
+        entries = by_step[s]
+        dev = []
+        for c, old, st, gold, gb in entries:
+            t = [torch.from_numpy(x.copy()).to(cuda_dev) for x in old]
+            gr = torch.from_numpy(gb.view(np.int16).copy()).view(torch.bfloat16).to(cuda_dev)
+            dev.append((t, gr, counter.next(F.Hparams(step=s + 1))))
+        # one call; runs of equal hp share a launch
+        from paper_2403_06504_b200._lib import LIB, AdamwArgs, check
+        import ctypes as C
+        arr = (AdamwArgs * len(dev))()
+        for i, (t, gr, hp) in enumerate(dev):
+            a = arr[i]
+            a.master, a.exp_avg, a.exp_avg_sq = (x.data_ptr() for x in t)
+            a.grad, a.grad_dtype, a.n, a.hp = gr.data_ptr(), 0, t[0].numel(), hp.c()
+        check(LIB.fy_adamw_chunks(arr, len(dev), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        torch.cuda.synchronize()
+        for (c, old, st, gold, gb), (t, gr, hp) in zip(entries, dev):
+            got = [x.cpu().numpy() for x in t]
+            for x, y in zip(got, st):
+                assert _bits_equal(x, y), f"step {s + 1} chunk {c} vs oracle"
+            trajectory_check(s, c, old, got, gold, gb)
