@@ -237,9 +237,7 @@ def cpu_oracle_rate(chunk: int, nchunks: int, target_s: float = 12.0, max_reps: 
     m = np.empty(n, np.float32)
     v = np.empty(n, np.float32)
     g = np.empty(n, np.uint16)
-    for a, val in ((master, 0.01), (m, 1e-4), (v, 1e-6)):
-        O.LIB.oracle_first_touch(a.ctypes.data, n, val, threads)
-    g[:] = 0x3A83  # bf16 ~1e-3
+    O.fill_s8d(master, m, v, g, threads=threads)  # SURVEY §8d distributions, first touch
     s = O.scalars()
     O.adamw_step_omp(master, m, v, g, O.BF16, s, param_out=g, threads=threads)  # warm
     reps, t0 = 0, time.perf_counter()
@@ -251,7 +249,7 @@ def cpu_oracle_rate(chunk: int, nchunks: int, target_s: float = 12.0, max_reps: 
             break
     rate = reps * n / el
     sample = (f"{nchunks} chunk(s) x {chunk} params (13B-shape block), {reps} passes, "
-              f"{el:.1f} s, bf16 grads->bf16 params in place")
+              f"{el:.1f} s, bf16 grads->bf16 params in place, SURVEY §8d input distributions")
     return rate, threads, sample
 
 
@@ -572,7 +570,12 @@ def resident_phase(torch, F, args, world, rank, local):
         st[c:2 * c].normal_(0, 1e-3, generator=gen)
         st[2 * c:].normal_(0, 1e-3, generator=gen).square_()
         states.append(st)
-        grads.append((torch.randn(c, device=dev, generator=gen) * 1e-3).to(torch.bfloat16))
+        # the reference's in-place convention: this rank's gradients sit in
+        # its slot of the shard's param arena and the update overwrites them
+        # with the params (14 B/param of HBM at N=1: C2 = 176 GB fits)
+        g = sh.own_params(k)
+        g.copy_((torch.randn(c, device=dev, generator=gen) * 1e-3).to(torch.bfloat16))
+        grads.append(g)
     io = [dict(states=states[k].data_ptr(), grad=grads[k].data_ptr()) for k in range(L)]
     stream = torch.cuda.current_stream(dev)
     hp = F.optim.Hparams()
@@ -1091,15 +1094,16 @@ def swap_engine_phase(torch, F, blocks_cpu=40, blocks_ssd=8):
     return out
 
 
-def swap_sweep_phase(F, budget_cpu=8e9, budget_ssd=2e9):
+def swap_sweep_phase(F, budget_cpu=32e9, budget_ssd=8e9):
     """BASELINE config 5: activation swap GPU->host(->SSD) bandwidth sweep,
     13B shape, s=2048, b in {8,16,32,64}, swap amounts chosen by the
     unchanged planner (a100 preset; coefficients 0/0/1/1, checkpoints on
     CPU). Executes the swap-only subgraph (offsim_execute swap_only) on a
     bounded number of blocks (host RAM / disk), once with the planner's
     placement (GPU->pinned host->GPU) and once forcing SSD placement
-    (GPU->host->file->host->GPU, O_DIRECT io_uring). Per-leg GB/s from the
-    real trace (bytes / busy time of the lane)."""
+    (GPU->host->file->host->GPU, O_DIRECT io_uring). Per leg: GB/s from the
+    real trace (bytes / summed durations of that leg's requests) and its
+    fraction of the peak the run measured on the same engine."""
     L = F.LIB
     P = C.c_void_p
     L.offsim_scenario_parse.argtypes = [C.c_char_p, C.POINTER(P)]
@@ -1130,24 +1134,25 @@ def swap_sweep_phase(F, budget_cpu=8e9, budget_ssd=2e9):
             d = json.loads(C.cast(summ, C.c_char_p).value.decode()) if summ.value else {}
             if summ.value:
                 L.offsim_string_free(summ)
-            busy = d.get("executed", {}).get("busy_s", {})
-            pb = d.get("physical_bytes", {})
+            # per leg: bytes and the summed durations of that leg's own
+            # requests in the real trace (the SSD lane's reads and writes are
+            # separate requests on a simplex lane, timed separately), against
+            # the peaks the run measured on the same engines: pinned 512 MiB
+            # copies (PCIe, each direction alone) and O_DIRECT io_uring
+            # requests through registered buffers (file tier)
+            rates = d.get("measured_rates", {})
             legs = {}
-            for leg, lane, key in (("gpu_to_host", "link_g2c", "d2h/activations"),
-                                   ("host_to_gpu", "link_c2g", "h2d/activations"),
-                                   ("host_to_ssd", "link_ssd", "file_write/activations"),
-                                   ("ssd_to_host", "link_ssd", "file_read/activations")):
-                if pb.get(key):
-                    legs[leg] = {"bytes": pb[key]}
-            if "host_to_ssd" in legs:  # the SSD lane is simplex: split its busy time by bytes
-                tot = legs["host_to_ssd"]["bytes"] + legs["ssd_to_host"]["bytes"]
-                for leg in ("host_to_ssd", "ssd_to_host"):
-                    legs[leg]["busy_s"] = busy.get("link_ssd", 0) * legs[leg]["bytes"] / tot
-            for leg, lane in (("gpu_to_host", "link_g2c"), ("host_to_gpu", "link_c2g")):
-                if leg in legs:
-                    legs[leg]["busy_s"] = busy.get(lane, 0)
-            for v in legs.values():
-                v["gbs"] = v["bytes"] / v["busy_s"] / 1e9 if v.get("busy_s") else None
+            for leg, key, peak in (("gpu_to_host", "link_g2c/g2c/activations", rates.get("d2h_bps")),
+                                   ("host_to_gpu", "link_c2g/c2g/activations", rates.get("h2d_bps")),
+                                   ("host_to_ssd", "link_ssd/c2s/activations", rates.get("file_write_bps")),
+                                   ("ssd_to_host", "link_ssd/s2c/activations", rates.get("file_read_bps"))):
+                lg = d.get("legs", {}).get(key)
+                if not lg:
+                    continue
+                gbs = lg["bytes"] / lg["busy_s"] / 1e9 if lg["busy_s"] else None
+                legs[leg] = {"bytes": lg["bytes"], "busy_s": lg["busy_s"], "requests": lg["requests"],
+                             "gbs": gbs, "peak_gbs": peak / 1e9 if peak else None,
+                             "frac": gbs / (peak / 1e9) if gbs and peak else None}
             rows.append({"batch": b, "placement": placement, "status": st,
                          "swap_coefficient": coef, "swapped_layers": plan["swapped_layer_count"],
                          "d_f_bytes": plan["d_f_bytes"], "checkpoint_location": d.get("checkpoint_location"),
@@ -1261,9 +1266,7 @@ def run_reference(args):
     m = np.empty(n, np.float32)
     v = np.empty(n, np.float32)
     g = np.empty(n, np.uint16)
-    for a, val in ((master, 0.01), (m, 1e-4), (v, 1e-6)):
-        O.LIB.oracle_first_touch(a.ctypes.data, n, val, threads)
-    g[:] = 0x3A83
+    O.fill_s8d(master, m, v, g, threads=threads)  # SURVEY §8d distributions, first touch
     s = O.scalars()
     for _ in range(args.warmup):
         O.adamw_step_omp(master, m, v, g, O.BF16, s, param_out=g, threads=threads)
@@ -1273,7 +1276,8 @@ def run_reference(args):
     el = time.perf_counter() - t0
     rate = args.steps * n / el
     sample = (f"each step: {nchunks} of the {args.layers} chunks ({N} params each, 13B shape), "
-              "bf16 grads -> bf16 params in place, DeepSpeed-0.9.3 CPU Adam restatement")
+              "bf16 grads -> bf16 params in place, SURVEY §8d input distributions, "
+              "DeepSpeed-0.9.3 CPU Adam restatement")
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,

@@ -186,6 +186,21 @@ HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRat
 // rank 3: analytic vs executed).
 HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const MeasuredRates& r);
 
+// The reference's analytic cost model (cost_model.cpp:26-90: t_iter =
+// t_f + t_bo, each phase the max over its lanes of work / rate) applied to
+// the B200-mapped graph: per phase (forward = "fwd ..." tasks; backward +
+// optimizer = "bwd ..." / "opt ..." tasks), the busiest lane's summed task
+// durations on `hw`. Same structure as iteration_time, but over the bytes
+// the B200 execution actually moves (state hops on the host link, resident
+// groups moving nothing), so it is comparable with an executed makespan.
+struct AnalyticTimes {
+    double t_f = 0.0;   // forward phase
+    double t_bo = 0.0;  // backward + optimizer phase
+    double t_iter = 0.0;
+    std::string bottleneck_f, bottleneck_bo;  // lane names
+};
+AnalyticTimes analytic_iteration(const TaskGraph& mapped, const HardwareConfig& hw);
+
 struct ExecReport {
     TaskGraph graph;        // the mapped graph that ran
     SimTrace trace;         // real timings (CUDA events), same type as simulate()
@@ -194,6 +209,9 @@ struct ExecReport {
     InvariantReport invariants;
     HardwareConfig hw_exec;
     HardwareConfig hw_predicted;
+    HardwareConfig hw_scenario;  // the scenario's own hardware (e.g. a persisted measured preset)
+    SimTrace scenario_predicted; // simulate() of the mapped graph on hw_scenario
+    MeasuredRates rates;         // the in-run calibration behind hw_exec / hw_predicted
     std::map<std::string, double> reference_bytes; // "<lane>/<payload>" of the input graph
     std::map<std::string, double> physical_bytes;  // "h2d|d2h|file_read|file_write/<payload>"
     double grad_sq_sum = 0.0;

@@ -60,6 +60,8 @@ def _load():
     lib.oracle_adamw_step_omp.restype = None
     lib.oracle_max_threads.restype = C.c_int
     lib.oracle_first_touch.argtypes = [vp, C.c_uint64, C.c_float, C.c_int]
+    lib.oracle_fill_s8d.argtypes = [vp, C.c_uint64, C.c_int, C.c_uint64, C.c_int]
+    lib.oracle_fill_s8d.restype = None
     lib.oracle_float_to_bf16.argtypes = [C.c_float]
     lib.oracle_float_to_bf16.restype = C.c_uint16
     lib.oracle_float_to_fp16.argtypes = [C.c_float]
@@ -128,6 +130,13 @@ def adamw_step_omp(master, m, v, grad, grad_dtype, s, grad_scale=1.0, param_out=
                    param_dtype=BF16, threads=0):
     LIB.oracle_adamw_step_omp(_p(master), _p(m), _p(v), _p(grad), grad_dtype, _p(param_out),
                               param_dtype, master.size, C.byref(s), grad_scale, threads)
+
+
+def fill_s8d(master, m, v, grad_bits, seed: int = 20240817, threads: int = 0) -> None:
+    """Parallel first-touch fill with SURVEY §8d's distributions (timing
+    samples for the CPU baseline; see oracle_fill_s8d)."""
+    for kind, a in enumerate((master, m, v, grad_bits)):
+        LIB.oracle_fill_s8d(_p(a), a.size, kind, seed, threads)
 
 
 def max_threads() -> int:

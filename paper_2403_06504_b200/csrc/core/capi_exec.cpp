@@ -166,6 +166,51 @@ json optimizer_json(const ExecReport& r) {
                 {"nonfinite", r.nonfinite}};
 }
 
+// Executed time and bytes per (lane, direction, payload) leg, from the real
+// trace: the SSD lane's reads and writes are timed as separate legs (each
+// event is one request's own duration), not split by bytes.
+json legs_json(const ExecReport& r) {
+    struct Leg {
+        double bytes = 0, busy_ns = 0, count = 0;
+    };
+    std::map<std::string, Leg> legs;
+    for (const TraceEvent& e : r.trace.events) {
+        if (e.dir == TransferDir::none || e.work <= 0.0) continue;
+        Leg& l = legs[std::string(to_string(e.resource)) + "/" + to_string(e.dir) + "/" + to_string(e.payload)];
+        l.bytes += e.work;
+        l.busy_ns += static_cast<double>(e.end_ns - e.start_ns);
+        l.count += 1;
+    }
+    json j = json::object();
+    for (const auto& [k, l] : legs)
+        j[k] = json{{"bytes", l.bytes}, {"busy_s", l.busy_ns * 1e-9}, {"requests", l.count},
+                    {"gbs", l.busy_ns > 0 ? l.bytes / l.busy_ns : 0.0}};
+    return j;
+}
+
+json rates_json(const MeasuredRates& m) {
+    return json{{"h2d_bps", m.h2d_bps},
+                {"d2h_bps", m.d2h_bps},
+                {"h2d_effective_bps", m.h2d_effective_bps},
+                {"d2h_effective_bps", m.d2h_effective_bps},
+                {"file_read_bps", m.file_read_bps},
+                {"file_write_bps", m.file_write_bps},
+                {"file_read_effective_bps", m.file_read_effective_bps},
+                {"file_write_effective_bps", m.file_write_effective_bps},
+                {"optimizer_params_per_s", m.optimizer_params_per_s},
+                {"compute_flops", m.compute_flops / m.compute_headroom}};
+}
+
+json analytic_json(const TaskGraph& g, const HardwareConfig& hw, double executed_s) {
+    const AnalyticTimes a = analytic_iteration(g, hw);
+    return json{{"t_f_s", a.t_f},
+                {"t_bo_s", a.t_bo},
+                {"t_iter_s", a.t_iter},
+                {"bottleneck_f", a.bottleneck_f},
+                {"bottleneck_bo", a.bottleneck_bo},
+                {"executed_over_analytic", a.t_iter > 0 ? executed_s / a.t_iter : 0.0}};
+}
+
 } // namespace
 
 std::string exec_summary_json(const ExecReport& r) {
@@ -175,6 +220,7 @@ std::string exec_summary_json(const ExecReport& r) {
     const HardwareConfig& h = r.hw_exec;
     const HardwareConfig& e = r.hw_predicted;
     const double pred_s = static_cast<double>(r.predicted.makespan_ns) * 1e-9;
+    const double exec_s = r.trace.makespan_s();
     const json doc = {
         {"schema_version", 1},
         {"command", "execute"},
@@ -191,6 +237,27 @@ std::string exec_summary_json(const ExecReport& r) {
         {"predicted", trace_stats(r.predicted)},
         {"executed_over_predicted",
          pred_s > 0 ? static_cast<double>(r.trace.makespan_ns) * 1e-9 / pred_s : 0.0},
+        {"measured_rates", rates_json(r.rates)},
+        // the calibration loop: analytic t_iter (reference cost-model
+        // structure) and the DES, on the in-run effective rates and on the
+        // scenario's own hardware (a persisted measured preset, or the
+        // modeled preset the plan was made on)
+        {"analytic", analytic_json(r.graph, e, exec_s)},
+        {"scenario_prediction",
+         json{{"hardware", r.hw_scenario.name},
+              {"des_makespan_s", r.scenario_predicted.makespan_s()},
+              {"executed_over_des", r.scenario_predicted.makespan_ns > 0
+                                        ? exec_s / r.scenario_predicted.makespan_s() : 0.0},
+              {"analytic", analytic_json(r.graph, r.hw_scenario, exec_s)}}},
+        // the invariant check's roofline uses hw_exec = measured burst rates
+        // x headroom (b200_hardware); the same bound on the effective rates,
+        // with no headroom, is reported beside it
+        {"roofline_check",
+         json{{"headroom", json{{"link", 1.05}, {"file", 1.5}, {"optimizer", 1.05}}},
+              {"bound_exec_s", static_cast<double>(roofline_lower_bound_ns(r.graph, r.hw_exec)) * 1e-9},
+              {"bound_effective_s", static_cast<double>(roofline_lower_bound_ns(r.graph, e)) * 1e-9},
+              {"executed_s", exec_s}}},
+        {"legs", legs_json(r)},
         {"optimizer", optimizer_json(r)},
         {"reference_bytes", bytes_json(r.reference_bytes)},
         {"physical_bytes", bytes_json(r.physical_bytes)},

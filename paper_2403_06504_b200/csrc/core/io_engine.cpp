@@ -33,10 +33,13 @@ T* at(void* base, std::uint32_t off) {
 
 } // namespace
 
-IoEngine::IoEngine(unsigned depth, std::uint64_t piece) : depth_(depth), piece_(piece) {
+IoEngine::IoEngine(unsigned depth, std::uint64_t piece)
+    // IORING_MAX_ENTRIES is 32768: io_depth x tier devices may exceed it
+    : depth_(std::min(std::max(depth, 1u), 32768u)), piece_(piece) {
     io_uring_params p;
     std::memset(&p, 0, sizeof p);
-    const int fd = uring_setup(depth, &p);
+    p.flags = IORING_SETUP_CLAMP;
+    const int fd = uring_setup(depth_, &p);
     if (fd < 0) return; // refused: fall back to pread/pwrite
     sq_len_ = p.sq_off.array + p.sq_entries * sizeof(unsigned);
     cq_len_ = p.cq_off.cqes + p.cq_entries * sizeof(io_uring_cqe);

@@ -312,3 +312,30 @@ HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const M
 }
 
 } // namespace offsim
+
+namespace offsim {
+
+AnalyticTimes analytic_iteration(const TaskGraph& mapped, const HardwareConfig& hw) {
+    // per phase, per lane: the summed durations the DES would charge
+    std::map<ResourceId, std::uint64_t> fwd, bwd;
+    for (const Task& t : mapped.tasks) {
+        const bool forward = t.name.rfind("fwd ", 0) == 0;
+        (forward ? fwd : bwd)[t.resource] += task_duration_ns(t, hw);
+    }
+    auto busiest = [](const std::map<ResourceId, std::uint64_t>& m, std::string& lane) {
+        std::uint64_t best = 0;
+        for (const auto& [r, ns] : m)
+            if (ns > best) {
+                best = ns;
+                lane = to_string(r);
+            }
+        return static_cast<double>(best) * 1e-9;
+    };
+    AnalyticTimes a;
+    a.t_f = busiest(fwd, a.bottleneck_f);
+    a.t_bo = busiest(bwd, a.bottleneck_bo);
+    a.t_iter = a.t_f + a.t_bo;
+    return a;
+}
+
+} // namespace offsim

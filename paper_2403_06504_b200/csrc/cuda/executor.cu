@@ -1252,6 +1252,9 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
     rep.planned = simulate(rep.graph, rep.hw_exec);
     rep.hw_predicted = b200_hardware_effective(hw, rates);
     rep.predicted = simulate(rep.graph, rep.hw_predicted);
+    rep.hw_scenario = hw;
+    rep.scenario_predicted = simulate(rep.graph, hw);
+    rep.rates = rates;
     eng.run(rep.planned, rep);
     rep.io_fixed_requests -= cal_fixed;  // the iteration's requests only
     rep.io_plain_requests -= cal_plain;

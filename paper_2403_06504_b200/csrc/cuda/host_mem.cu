@@ -88,10 +88,26 @@ int host_numa_node(const void* p) {
     return status;  // node, or -errno for an unpopulated page
 }
 
+std::uint64_t host_mem_available() {
+    std::ifstream f("/proc/meminfo");
+    std::string key;
+    std::uint64_t kb = 0;
+    std::string unit;
+    while (f >> key >> kb) {
+        std::getline(f, unit);
+        if (key == "MemAvailable:") return kb * 1024ull;
+    }
+    return ~0ull;  // unknown: let mmap / cudaHostRegister decide
+}
+
 void* host_alloc(std::uint64_t bytes, int node, int* placed) {
     const std::uint64_t len = round_up(std::max<std::uint64_t>(bytes, 1), kHuge);
-    void* p = ::mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE,
-                     -1, 0);
+    // populate() touches every page, so an oversized request would be
+    // OOM-killed instead of failing: refuse it here (nullptr -> the caller's
+    // FY_ERR_INFEASIBLE / cudaHostAlloc fallback), keeping 1 GiB of headroom.
+    const std::uint64_t avail = host_mem_available();
+    if (avail != ~0ull && len + (1ull << 30) > avail) return nullptr;
+    void* p = ::mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p == MAP_FAILED) return nullptr;
     ::madvise(p, len, MADV_HUGEPAGE);  // fewer pages to pin (best effort)
     bool bound = false;

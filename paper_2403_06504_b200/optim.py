@@ -349,12 +349,29 @@ class Shard:
         check(LIB.fy_shard_create(C.byref(cfg), C.byref(h)))
         self._h = h
         self._io = None
+        self._param_dtype, self._device = param_dtype, device
         self.world, self.rank = world, rank
 
     def slice(self, c: int) -> dict:
         s = ShardSlice()
         check(LIB.fy_shard_slice_info(self._h, c, C.byref(s)))
         return dict(offset=s.offset, count=s.count, stride=s.stride, params=s.params)
+
+    def own_params(self, c: int) -> torch.Tensor:
+        """This rank's slot of chunk c's full params in the arena (16-bit,
+        `count` elements): the in-place buffer of the reference's convention
+        (the update writes the params into the grad buffer,
+        proj/src/task_graph.cpp:493-495). A caller that lands the slice's
+        gradients here (io grad = this tensor, grad_dtype 16-bit) needs no
+        separate gradient memory: 2 B/param of HBM saved."""
+        s = self.slice(c)
+        dt = self._param_dtype
+        if s["count"] == 0:
+            return torch.empty(0, dtype=dt, device=torch.device("cuda", self._device))
+        ptr = s["params"] + self.rank * s["stride"] * 2
+        cai = type("CAI", (), {"__cuda_array_interface__": dict(
+            shape=(s["count"],), typestr="<i2", data=(ptr, False), version=3)})()
+        return torch.as_tensor(cai, device=torch.device("cuda", self._device)).view(dt)
 
     def ipc_handle(self) -> bytes:
         buf = C.create_string_buffer(FY_IPC_HANDLE_BYTES)

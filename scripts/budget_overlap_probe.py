@@ -76,6 +76,51 @@ def timed(fn, reps=3):
     return best
 
 
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _NV = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+except Exception:  # noqa: BLE001
+    _NV = None
+
+
+def powered(fn, seconds=2.0):
+    """Run fn back to back for ~seconds; NVML board power (median, W) and
+    SM clock sampled every 10 ms, energy per call = mean power x time per
+    call (J). The energy bookkeeping behind the power-cap reading."""
+    import threading
+    import time
+    ms = timed(fn, reps=2)
+    reps = max(3, int(seconds * 1e3 / ms))
+    samples, stop = [], threading.Event()
+
+    def sample():
+        while not stop.is_set():
+            samples.append((pynvml.nvmlDeviceGetPowerUsage(_NV) / 1e3,
+                            pynvml.nvmlDeviceGetClockInfo(_NV, pynvml.NVML_CLOCK_SM)))
+            time.sleep(0.01)
+    th = threading.Thread(target=sample) if _NV is not None else None
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if th:
+        th.start()
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    if th:
+        stop.set()
+        th.join()
+    per = a.elapsed_time(b) / reps
+    steady = samples[len(samples) // 3:] if samples else []
+    pw = sorted(x[0] for x in steady)
+    mhz = sorted(x[1] for x in steady)
+    p_med = pw[len(pw) // 2] if pw else None
+    return {"ms": per, "power_w": p_med, "sm_mhz": mhz[len(mhz) // 2] if mhz else None,
+            "energy_j": p_med * per * 1e-3 if p_med else None}
+
+
 def emit(d):
     print(json.dumps(d), flush=True)
 
@@ -124,3 +169,45 @@ if "overlap" in PHASES:
                   "hidden_fraction_vs_full_gpu_serial": (t_bwd_full + t_opt_full - t_both) / t_opt_full})
     torch._C._set_sm_carveout_experimental(0)
     check(LIB.fy_adamw_sm_budget(0))
+
+if "power" in PHASES:
+    # energy bookkeeping under the board power cap: if the backward and the
+    # update each run AT the cap alone, running them together cannot take
+    # less than (E_backward + E_update - P_idle x t) / P_cap
+    idle = None
+    if _NV is not None:
+        import time
+        torch.cuda.synchronize()
+        time.sleep(1.0)
+        idle = pynvml.nvmlDeviceGetPowerUsage(_NV) / 1e3
+        cap = pynvml.nvmlDeviceGetEnforcedPowerLimit(_NV) / 1e3
+    else:
+        cap = None
+
+    def both_on(opt_stream_fn):
+        cur = torch.cuda.current_stream()
+        bwd_s.wait_stream(cur)
+        opt_s.wait_stream(cur)
+        for k in range(K):
+            with torch.cuda.stream(bwd_s):
+                bwd_block()
+                e = torch.cuda.Event()
+                e.record(bwd_s)
+            opt_s.wait_event(e)
+            opt_block(k, opt_s)
+        cur.wait_stream(bwd_s)
+        cur.wait_stream(opt_s)
+
+    for path, label in ((1, "tma"), (0, "lsu")):
+        check(LIB.fy_adamw_tune(path, 0, 0))
+        check(LIB.fy_adamw_sm_budget(0))
+        b = powered(lambda: [bwd_block() for _ in range(K)])
+        o = powered(lambda: [opt_block(k, torch.cuda.current_stream()) for k in range(K)])
+        c = powered(lambda: both_on(None))
+        emit({"probe": "power", "path": label, "idle_w": idle, "cap_w": cap,
+              "backward": b, "optimizer": o, "both": c,
+              "serial_ms": b["ms"] + o["ms"],
+              "hidden_fraction": (b["ms"] + o["ms"] - c["ms"]) / o["ms"],
+              "energy_bound_ms": ((b["energy_j"] + o["energy_j"]) / cap * 1e3
+                                  if cap and b["energy_j"] and o["energy_j"] else None)})
+    check(LIB.fy_adamw_tune(1, 0, 0))

@@ -17,6 +17,10 @@ cases = {
     "c1_b128": (X.scenario(batch=128), {"tier": "host", "compute_rate": 1.4e15}),
     "13b_4blk": (X.scenario(layers=4, heads=40, hidden=5120, batch=8, name="13b4"),
                  {"tier": "host", "compute_mode": "gemm"}),
+    "c1_b8_resident": (X.scenario(batch=8), {"tier": "host", "compute_rate": 1.4e15,
+                                             "resident_groups": "all"}),
+    "13b_4blk_resident": (X.scenario(layers=4, heads=40, hidden=5120, batch=8, name="13b4"),
+                          {"tier": "host", "compute_mode": "gemm_dataflow", "resident_groups": "all"}),
 }
 # args: [tag ...] [--opts JSON] (extra ExecOptions merged into every case)
 args = sys.argv[1:]
@@ -31,4 +35,5 @@ for tag in (args or list(cases)):
     st, summ, trace, err = X.execute(sc, opts, want_trace=True)
     (out / f"exec_{tag}_summary.json").write_text(json.dumps(summ, indent=1))
     (out / f"exec_{tag}_trace.json").write_text(trace or "")
+    (out / f"exec_{tag}_scenario.json").write_text(sc)
     print(tag, st, err, summ["executed"]["makespan_s"], summ["planned"]["makespan_s"])

@@ -30,8 +30,12 @@ def test_cli_execute_writes_valid_executed_trace(cuda_dev, tmp_path, variant):
     sc.write_text(scenario(variant=variant))
     tr = tmp_path / "t.json"
     out = tmp_path / "summary.json"
+    # the pipelined variant stages gradients through the SSD tier: files
+    opts = {"tier": "host", "compute_rate": 1.4e15}
+    if variant == "pipelined":
+        opts = {"tier": "file", "file_dir": str(tmp_path / "tier"), "compute_rate": 1.4e15}
     r = subprocess.run([str(EXE), "execute", "--scenario", str(sc), "--exec",
-                        json.dumps({"tier": "host", "compute_rate": 1.4e15}), "--trace", str(tr),
+                        json.dumps(opts), "--trace", str(tr),
                         "--out", str(out)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     s = json.loads(out.read_text())

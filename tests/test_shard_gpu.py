@@ -160,6 +160,20 @@ def test_shard_single_process_peer_world8(cuda_dev):
     assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-3000:]
 
 
+def _raw_streams(n):
+    """Caller streams made with the runtime directly: torch.cuda.Stream()
+    would initialise torch's pools (32 streams per priority) and, past
+    CUDA_DEVICE_MAX_CONNECTIONS hardware queues, streams share a queue — a
+    spinning device barrier then blocks the very peer it waits for."""
+    from cuda.bindings import runtime as rt
+    out = []
+    for _ in range(n):
+        err, h = rt.cudaStreamCreateWithFlags(rt.cudaStreamNonBlocking)
+        assert err == rt.cudaError_t.cudaSuccess, err
+        out.append(torch.cuda.ExternalStream(int(h)))
+    return out
+
+
 def single_process_peer(cuda_dev, world, tier):
     from paper_2403_06504_b200 import optim as F
     inp = _inputs(SIZES, seed=world)
@@ -169,7 +183,7 @@ def single_process_peer(cuda_dev, world, tier):
     for s in shards:
         s.connect_ptrs(arenas)
     bufs = [_shard_buffers(F, s, inp, cuda_dev, tier) for s in shards]
-    streams = [torch.cuda.Stream() for _ in shards]
+    streams = _raw_streams(len(shards))
     steps = (10, 11)
     ref, sqs = _oracle(inp, steps)
     for i, step in enumerate(steps):

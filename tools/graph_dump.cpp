@@ -10,7 +10,7 @@
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::cerr << "usage: graph_dump scenario.json\n";
+        std::cerr << "usage: graph_dump scenario.json [resident_groups|all]\n";
         return 2;
     }
     std::ifstream f(argv[1]);
@@ -19,7 +19,9 @@ int main(int argc, char** argv) {
     const offsim::Scenario s = offsim::load_scenario(ss.str());
     const offsim::SwapPlan plan = offsim::plan_for_scenario(s);
     const offsim::TaskGraph ref = offsim::build_schedule(s.model, s.hardware, plan, s.variant);
-    offsim::TaskGraph g = offsim::map_graph_for_b200(ref, offsim::StateTier::host, 3);
+    std::uint32_t resident = 0;
+    if (argc > 2) resident = std::string(argv[2]) == "all" ? 0xffffffffu : static_cast<std::uint32_t>(std::stoul(argv[2]));
+    offsim::TaskGraph g = offsim::map_graph_for_b200(ref, offsim::StateTier::host, 3, resident);
     offsim::ExecOptions o;
     offsim::add_host_ring_edges(g, offsim::host_ring_depths(g, o));
     std::cout << "[\n";
