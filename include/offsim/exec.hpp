@@ -100,6 +100,11 @@ struct ExecOptions {
     // map_graph_for_b200); 0xffffffff = all groups ("all"); kResidentAuto =
     // as many as the HBM left after the executor's own buffers holds ("auto").
     std::uint32_t resident_groups = 0;
+    // "graph": the iteration is captured once into one CUDA graph and
+    // launched as a unit (no host issue latency between tasks; falls back to
+    // "stream" if the capture is refused); "stream": tasks issued one by one
+    // on the lane streams in planned start order
+    std::string launch = "graph";
 };
 
 inline constexpr std::uint32_t kResidentAuto = 0xfffffffeu;
@@ -232,6 +237,7 @@ struct ExecReport {
     RingDepths host_ring;                 // staging ring depths (file tier)
     std::uint64_t state_checksum = 0;     // checksum_states
     std::uint32_t resident_groups = 0;    // optimizer groups kept in HBM
+    std::string launch_mode;              // "graph" | "stream" (what actually ran)
 };
 
 ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const SwapPlan& plan,

@@ -43,7 +43,8 @@ ParsedOptions parse_options(const char* text) {
                                                "verify_swaps", "adam", "dry_run", "variant",
                                                "swap_only", "max_blocks", "placement",
                                                "compute_mode", "host_ring", "checksum_states",
-                                               "resident_groups", "fixed_buffers", "io_depth"};
+                                               "resident_groups", "fixed_buffers", "io_depth",
+                                               "launch"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -67,6 +68,9 @@ ParsedOptions parse_options(const char* text) {
         o.direct_io = doc.value("direct_io", o.direct_io);
         o.fixed_buffers = doc.value("fixed_buffers", o.fixed_buffers);
         o.io_depth = doc.value("io_depth", o.io_depth);
+        o.launch = doc.value("launch", o.launch);
+        if (o.launch != "graph" && o.launch != "stream")
+            throw ConfigError("exec options: launch must be \"graph\" or \"stream\"");
         if (o.io_depth < 1 || o.io_depth > 1024) throw ConfigError("exec options: io_depth must be 1..1024");
         o.compute_rate = doc.value("compute_rate", o.compute_rate);
         o.state_slots = doc.value("state_slots", o.state_slots);
@@ -273,6 +277,7 @@ std::string exec_summary_json(const ExecReport& r) {
         {"host_ring", rings_json(r.host_ring)},
         {"state_checksum", r.state_checksum},
         {"resident_groups", r.resident_groups},
+        {"launch", r.launch_mode},
         {"invariants", checks},
         {"all_invariants_pass", r.invariants.all_pass && r.swap_mismatches == 0},
     };

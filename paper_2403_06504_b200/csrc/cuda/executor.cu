@@ -275,6 +275,7 @@ public:
         (void)g_io_done.load(std::memory_order_acquire);
         if (blas_) cublasDestroy(blas_);
         for (cudaEvent_t e : events_) cudaEventDestroy(e);
+        for (cudaEvent_t e : deps_) cudaEventDestroy(e);
         if (base_) cudaEventDestroy(base_);
         for (cudaStream_t s : streams_)
             if (s) cudaStreamDestroy(s);
@@ -341,8 +342,19 @@ private:
     void assign_ring_slots();
 
     cudaStream_t streams_[5] = {};
-    std::vector<cudaEvent_t> events_;
+    std::vector<cudaEvent_t> events_;  // [2 id]: start, [2 id + 1]: end (timing)
+    std::vector<cudaEvent_t> deps_;    // graph mode: task end, dependency only
     cudaEvent_t base_ = nullptr;
+    bool capturing_ = false;           // issue() is being captured into a CUDA graph
+    void record_time(cudaEvent_t e, cudaStream_t s) {
+        // in a capture an external record becomes an event-record NODE that
+        // timestamps when the graph executes (a plain record only marks a
+        // capture dependency)
+        check_cuda(capturing_ ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s),
+                   "record");
+    }
+    cudaEvent_t end_dep(std::uint32_t id) const { return capturing_ ? deps_[id] : events_[2 * id + 1]; }
+    bool run_graph(const std::vector<std::pair<std::uint64_t, std::uint32_t>>& order, ExecReport& rep);
 
     // host side
     std::vector<Pinned> own_states_, own_params_, act_host_, ckpt_host_, grad_host_;
@@ -429,6 +441,8 @@ void Engine::setup() {
     }
     events_.resize(2 * g_.tasks.size());
     for (cudaEvent_t& e : events_) check_cuda(cudaEventCreate(&e), "event");
+    deps_.resize(g_.tasks.size());
+    for (cudaEvent_t& e : deps_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     check_cuda(cudaEventCreate(&base_), "event");
 
     const std::uint64_t state_b = 12 * n_, param_b = 2 * n_;
@@ -1006,7 +1020,7 @@ void Engine::issue(const Task& t, ExecReport& rep) {
     cudaStream_t s = lane_stream(t.resource);
     for (const std::uint32_t d : t.deps)
         if (g_.tasks[d].resource != t.resource)
-            check_cuda(cudaStreamWaitEvent(s, events_[2 * d + 1], 0), "wait dep");
+            check_cuda(cudaStreamWaitEvent(s, end_dep(d), 0), "wait dep");
     const Parsed p = parse_name(t.name);
     const std::uint32_t k = p.block;
     const int j = p.layer;
@@ -1030,7 +1044,7 @@ void Engine::issue(const Task& t, ExecReport& rep) {
         phys(write ? "file_write" : "file_read", bytes);
     };
 
-    check_cuda(cudaEventRecord(events_[2 * t.id], s), "record");
+    record_time(events_[2 * t.id], s);
     const std::uint64_t state_b = 12 * n_, param_b = 2 * n_;
     const std::string& w = p.what;
     if (t.work <= 0.0) {
@@ -1124,7 +1138,68 @@ void Engine::issue(const Task& t, ExecReport& rep) {
     } else {
         throw InvariantError("executor: no operation for task '" + t.name + "'");
     }
-    check_cuda(cudaEventRecord(events_[2 * t.id + 1], s), "record");
+    record_time(events_[2 * t.id + 1], s);
+    if (capturing_) check_cuda(cudaEventRecord(deps_[t.id], s), "record dep");
+}
+
+// Graph mode: the whole iteration captured once into ONE CUDA graph (lane
+// streams forked from / joined into streams_[0]; cross-lane dependencies are
+// graph edges; each task's start / end are event-record nodes), instantiated
+// before the timed region and launched as one unit. The GPU then resolves
+// every dependency itself: no host issue latency between tasks (stream mode
+// issues ~5 API calls per task from one host thread, which bounds small
+// iterations — C1 with HBM-resident states was host-issue bound, r02d).
+bool Engine::run_graph(const std::vector<std::pair<std::uint64_t, std::uint32_t>>& order, ExecReport& rep) {
+    const ExecReport saved = rep;
+    const std::size_t io_mark = io_reqs_.size();
+    const int turn = wscratch_turn_;
+    cudaStream_t origin = streams_[0];
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t fork = nullptr;
+    bool ok = false;
+    try {
+        check_cuda(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
+        check_cuda(cudaStreamBeginCapture(origin, cudaStreamCaptureModeRelaxed), "begin capture");
+        capturing_ = true;
+        record_time(base_, origin);
+        check_cuda(cudaEventRecord(fork, origin), "fork");
+        for (int r = 1; r < 5; ++r) check_cuda(cudaStreamWaitEvent(streams_[r], fork, 0), "fork wait");
+        for (const auto& [start, id] : order) issue(g_.tasks[id], rep);
+        for (int r = 1; r < 5; ++r) {  // join every lane back into the origin
+            check_cuda(cudaEventRecord(fork, streams_[r]), "join");
+            check_cuda(cudaStreamWaitEvent(origin, fork, 0), "join wait");
+        }
+        capturing_ = false;
+        check_cuda(cudaStreamEndCapture(origin, &graph), "end capture");
+        check_cuda(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+        check_cuda(cudaGraphUpload(exec, origin), "graph upload");
+        check_cuda(cudaStreamSynchronize(origin), "graph upload sync");
+        check_cuda(cudaGraphLaunch(exec, origin), "graph launch");
+        check_cuda(cudaStreamSynchronize(origin), "graph run");
+        ok = true;
+    } catch (const std::exception&) {
+        if (capturing_) {  // abandon the capture; the stream leaves capture mode
+            capturing_ = false;
+            cudaGraph_t partial = nullptr;
+            cudaStreamEndCapture(origin, &partial);
+            if (partial) cudaGraphDestroy(partial);
+        }
+        cudaGetLastError();
+        if (exec) {  // failed while running: a real device error, not a capture limit
+            cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+            if (fork) cudaEventDestroy(fork);
+            throw;
+        }
+        rep = saved;  // the stream-mode issue starts from a clean report
+        io_reqs_.resize(io_mark);
+        wscratch_turn_ = turn;
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (fork) cudaEventDestroy(fork);
+    return ok;
 }
 
 void Engine::run(const SimTrace& planned, ExecReport& rep) {
@@ -1136,9 +1211,14 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
     std::sort(order.begin(), order.end());
 
     check_cuda(cudaDeviceSynchronize(), "pre-run sync");
-    check_cuda(cudaEventRecord(base_, streams_[0]), "base");
-    for (int r = 1; r < 5; ++r) check_cuda(cudaStreamWaitEvent(streams_[r], base_, 0), "base wait");
-    for (const auto& [start, id] : order) issue(g_.tasks[id], rep);
+    rep.launch_mode = "stream";
+    if (opt_.launch == "graph" && run_graph(order, rep)) {
+        rep.launch_mode = "graph";
+    } else {
+        check_cuda(cudaEventRecord(base_, streams_[0]), "base");
+        for (int r = 1; r < 5; ++r) check_cuda(cudaStreamWaitEvent(streams_[r], base_, 0), "base wait");
+        for (const auto& [start, id] : order) issue(g_.tasks[id], rep);
+    }
     check_cuda(cudaDeviceSynchronize(), "executor run");
     (void)g_io_done.load(std::memory_order_acquire);  // pairs with run_io's release
     if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);

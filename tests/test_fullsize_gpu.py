@@ -10,7 +10,8 @@ properties:
 * C4 — one GPT-3-175B block (12*12288^2 = 1,811,939,328 params) sharded
   across 8 simulated ranks (fy_shard_range slices, fused all-gather epilogue
   into 8 full-param buffers) equals the single-launch step on the whole
-  chunk, bit for bit, in every rank's buffer.
+  chunk, bit for bit, in every rank's buffer, and the CPU oracle in windows
+  at the chunk's ends and straddling every rank boundary.
 """
 import numpy as np
 import pytest
@@ -41,10 +42,11 @@ def _same_bits(a: torch.Tensor, b: torch.Tensor) -> bool:
     return bool(torch.equal(a.view(view), b.view(view)))
 
 
-def _oracle_windows(n, st0, grad, st1, param, hp_step):
-    """Windows [0, W), the middle and the last W elements vs the oracle."""
+def _oracle_windows(n, st0, grad, st1, param, hp_step, los=None):
+    """Windows [0, W), the middle and the last W elements (or `los`) vs the
+    oracle."""
     sc = O.scalars(step=hp_step)
-    for lo in (0, n // 2 - WINDOW // 2, n - WINDOW):
+    for lo in (los or (0, n // 2 - WINDOW // 2, n - WINDOW)):
         sl = slice(lo, lo + WINDOW)
         mst = st0[:n][sl].cpu().numpy().copy()
         mm = st0[n:2 * n][sl].cpu().numpy().copy()
@@ -89,6 +91,12 @@ def test_c4_175b_block_sharded_8_equals_single(cuda_dev):
     from paper_2403_06504_b200 import optim as F
     n, world = N_175B, 8
     st, grad = _states(n, cuda_dev, 175)
+    # oracle windows: the chunk's first and last W elements and one window
+    # straddling every rank boundary of the 8-way slicing
+    bounds = [F.shard_range(n, world, r, 8)[0] for r in range(1, world)]
+    los = [0, n - WINDOW] + [b - WINDOW // 2 for b in bounds]
+    win0 = {lo: (st[lo:lo + WINDOW].clone(), st[n + lo:n + lo + WINDOW].clone(),
+                 st[2 * n + lo:2 * n + lo + WINDOW].clone(), grad[lo:lo + WINDOW].clone()) for lo in los}
     single = st.clone()
     p_single = torch.empty(n, dtype=torch.bfloat16, device=cuda_dev)
     hp = F.Hparams()
@@ -108,6 +116,18 @@ def test_c4_175b_block_sharded_8_equals_single(cuda_dev):
     assert _same_bits(st, single), "sharded states differ from the single launch"
     for r, b in enumerate(full + [local]):
         assert _same_bits(b, p_single), f"rank buffer {r} differs"
+    # the sharded result against the CPU oracle in the windows
+    sc = O.scalars(step=hp.step)
+    for lo, (m0, mm0, vv0, g0) in win0.items():
+        mst, mm, vv = (x.cpu().numpy().copy() for x in (m0, mm0, vv0))
+        g = g0.cpu().view(torch.int16).numpy().view(np.uint16).copy()
+        p = np.zeros(WINDOW, np.uint16)
+        O.adamw_step(mst, mm, vv, g, O.BF16, sc, param_out=p)
+        sl = slice(lo, lo + WINDOW)
+        for got, ref in ((st[:n][sl], mst), (st[n:2 * n][sl], mm), (st[2 * n:][sl], vv)):
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), ref.view(np.uint32)), lo
+        for b in full:
+            assert np.array_equal(b[sl].cpu().view(torch.int16).numpy().view(np.uint16), p), lo
 
 
 N_HUGE = (1 << 32) + 3 * 2048 + 5  # one chunk past 2^32 elements (60 GB of states + grads)
