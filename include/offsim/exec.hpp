@@ -171,6 +171,9 @@ struct MeasuredRates {
     double optimizer_params_per_s = 0.0;
     double compute_flops = 0.0;
     double compute_headroom = 1.0;  // compute_flops = measured x this (gemm mode)
+    // the graph's own compute tasks replayed back to back (per-kernel
+    // overhead and small-GEMM efficiency included)
+    double compute_effective_flops = 0.0;
     std::uint64_t gpu_mem = 0;
     std::uint64_t cpu_mem = 0;
     // Delivered link rates when this graph's own host<->device copies run
@@ -179,6 +182,16 @@ struct MeasuredRates {
     // rates above.
     double h2d_effective_bps = 0.0;
     double d2h_effective_bps = 0.0;
+    // the same copies replayed one direction at a time (per-copy overhead,
+    // no duplex contention)
+    double h2d_simplex_effective_bps = 0.0;
+    double d2h_simplex_effective_bps = 0.0;
+    // share of each link lane's planned busy time during which the other
+    // direction is also busy (link_overlap on the planned trace); the
+    // effective rate of a lane blends its simplex and duplex replays by it
+    double c2g_overlap = 1.0;
+    double g2c_overlap = 1.0;
+    double c2g_bytes = 0.0, g2c_bytes = 0.0;  // planned bytes per lane
     // file tier: this graph's own file-lane operations replayed in task order
     double file_read_effective_bps = 0.0;
     double file_write_effective_bps = 0.0;
@@ -190,6 +203,9 @@ HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRat
 // reference's DES on these predicts the executed makespan (SURVEY §8f
 // rank 3: analytic vs executed).
 HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const MeasuredRates& r);
+// Fills r.c2g_overlap / g2c_overlap / c2g_bytes / g2c_bytes from a trace of
+// `graph` (the DES on the burst rates: where the two copy directions overlap).
+void link_overlap(const TaskGraph& graph, const SimTrace& trace, MeasuredRates& r);
 
 // The reference's analytic cost model (cost_model.cpp:26-90: t_iter =
 // t_f + t_bo, each phase the max over its lanes of work / rate) applied to

@@ -197,12 +197,17 @@ json rates_json(const MeasuredRates& m) {
                 {"d2h_bps", m.d2h_bps},
                 {"h2d_effective_bps", m.h2d_effective_bps},
                 {"d2h_effective_bps", m.d2h_effective_bps},
+                {"h2d_simplex_effective_bps", m.h2d_simplex_effective_bps},
+                {"d2h_simplex_effective_bps", m.d2h_simplex_effective_bps},
+                {"c2g_overlap", m.c2g_overlap},
+                {"g2c_overlap", m.g2c_overlap},
                 {"file_read_bps", m.file_read_bps},
                 {"file_write_bps", m.file_write_bps},
                 {"file_read_effective_bps", m.file_read_effective_bps},
                 {"file_write_effective_bps", m.file_write_effective_bps},
                 {"optimizer_params_per_s", m.optimizer_params_per_s},
-                {"compute_flops", m.compute_flops / m.compute_headroom}};
+                {"compute_flops", m.compute_flops / m.compute_headroom},
+                {"compute_effective_flops", m.compute_effective_flops}};
 }
 
 json analytic_json(const TaskGraph& g, const HardwareConfig& hw, double executed_s) {

@@ -297,17 +297,28 @@ HardwareConfig b200_hardware(const HardwareConfig& planned_on, const MeasuredRat
 HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const MeasuredRates& r) {
     HardwareConfig hw = b200_hardware(planned_on, r);
     hw.name = "b200-effective";
+    // per direction: the graph's own copies replayed alone (simplex) and
+    // with the other direction running (duplex), blended per byte by the
+    // share of the lane's planned busy time the other direction overlaps
+    auto blend = [](double simplex, double duplex, double burst, double f) {
+        if (simplex <= 0) simplex = duplex > 0 ? duplex : burst;
+        if (duplex <= 0) duplex = simplex;
+        f = std::clamp(f, 0.0, 1.0);
+        return 1.0 / ((1.0 - f) / simplex + f / duplex);
+    };
+    const double up = blend(r.h2d_simplex_effective_bps, r.h2d_effective_bps, r.h2d_bps, r.c2g_overlap);
+    const double down = blend(r.d2h_simplex_effective_bps, r.d2h_effective_bps, r.d2h_bps, r.g2c_overlap);
     // one bw_gpu serves both link lanes in the reference's model
-    // (simulator.cpp:17-35): take the slower delivered direction
-    const double eff = std::min(r.h2d_effective_bps > 0 ? r.h2d_effective_bps : r.h2d_bps,
-                                r.d2h_effective_bps > 0 ? r.d2h_effective_bps : r.d2h_bps);
-    hw.bw_gpu = eff;
+    // (simulator.cpp:17-35): the rate of the lane that carries more bytes
+    // (the binding one; the other lane then finishes early either way)
+    hw.bw_gpu = r.c2g_bytes >= r.g2c_bytes ? up : down;
+    if (r.c2g_bytes <= 0 && r.g2c_bytes <= 0) hw.bw_gpu = std::min(up, down);
     if (r.file_read_bps > 0)
         hw.bw_s2c = r.file_read_effective_bps > 0 ? r.file_read_effective_bps : r.file_read_bps;
     if (r.file_write_bps > 0)
         hw.bw_c2s = r.file_write_effective_bps > 0 ? r.file_write_effective_bps : r.file_write_bps;
     hw.cpu_opt_tput = r.optimizer_params_per_s;
-    hw.gpu_tput = r.compute_flops / r.compute_headroom;
+    hw.gpu_tput = r.compute_effective_flops > 0 ? r.compute_effective_flops : r.compute_flops / r.compute_headroom;
     return hw;
 }
 
@@ -336,6 +347,46 @@ AnalyticTimes analytic_iteration(const TaskGraph& mapped, const HardwareConfig& 
     a.t_bo = busiest(bwd, a.bottleneck_bo);
     a.t_iter = a.t_f + a.t_bo;
     return a;
+}
+
+} // namespace offsim
+
+namespace offsim {
+
+void link_overlap(const TaskGraph& graph, const SimTrace& trace, MeasuredRates& r) {
+    // busy intervals per link lane (a lane is serial: its events do not overlap)
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> up, down;
+    double ub = 0, db = 0;
+    for (const TraceEvent& e : trace.events) {
+        if (e.end_ns <= e.start_ns) continue;
+        if (e.resource == ResourceId::link_c2g) {
+            up.emplace_back(e.start_ns, e.end_ns);
+            ub += graph.tasks[e.task_id].work;
+        } else if (e.resource == ResourceId::link_g2c) {
+            down.emplace_back(e.start_ns, e.end_ns);
+            db += graph.tasks[e.task_id].work;
+        }
+    }
+    std::sort(up.begin(), up.end());
+    std::sort(down.begin(), down.end());
+    auto total = [](const std::vector<std::pair<std::uint64_t, std::uint64_t>>& v) {
+        double t = 0;
+        for (const auto& [a, b] : v) t += static_cast<double>(b - a);
+        return t;
+    };
+    double both = 0;
+    for (std::size_t i = 0, j = 0; i < up.size() && j < down.size();) {
+        const std::uint64_t lo = std::max(up[i].first, down[j].first);
+        const std::uint64_t hi = std::min(up[i].second, down[j].second);
+        if (hi > lo) both += static_cast<double>(hi - lo);
+        if (up[i].second < down[j].second) ++i;
+        else ++j;
+    }
+    const double tu = total(up), td = total(down);
+    r.c2g_overlap = tu > 0 ? both / tu : 0.0;
+    r.g2c_overlap = td > 0 ? both / td : 0.0;
+    r.c2g_bytes = ub;
+    r.g2c_bytes = db;
 }
 
 } // namespace offsim

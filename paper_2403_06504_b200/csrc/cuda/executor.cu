@@ -295,6 +295,7 @@ public:
 private:
     cudaStream_t lane_stream(ResourceId r) const { return streams_[static_cast<int>(r)]; }
     void issue(const Task& t, ExecReport& rep);
+    void issue_compute(const Task& t, const Parsed& p, cudaStream_t s, bool replay);
     std::uint64_t layer_offset(int j) const; // byte offset of layer j inside the block params
 
     const ModelConfig& model_;
@@ -764,6 +765,26 @@ MeasuredRates Engine::calibrate() {
             }
             if (up_b > 0) r.h2d_effective_bps = up_b / best_u;
             if (down_b > 0) r.d2h_effective_bps = down_b / best_d;
+            // the same copies one direction at a time
+            auto simplex = [&](cudaStream_t st, const std::vector<std::uint64_t>& sizes, bool h2d) {
+                double best = 1e30;
+                for (int it = 0; it < 2 && !sizes.empty(); ++it) {
+                    check_cuda(cudaDeviceSynchronize(), "sync");
+                    check_cuda(cudaEventRecord(go, st), "record");
+                    for (const std::uint64_t b : sizes)
+                        check_cuda(h2d ? cudaMemcpyAsync(du.p, hu.p, b, cudaMemcpyHostToDevice, st)
+                                       : cudaMemcpyAsync(hd.p, dd.p, b, cudaMemcpyDeviceToHost, st),
+                                   "simplex replay");
+                    check_cuda(cudaEventRecord(eu, st), "record");
+                    check_cuda(cudaEventSynchronize(eu), "sync");
+                    float ms = 0;
+                    check_cuda(cudaEventElapsedTime(&ms, go, eu), "elapsed");
+                    best = std::min(best, ms * 1e-3);
+                }
+                return best;
+            };
+            if (up_b > 0) r.h2d_simplex_effective_bps = up_b / simplex(su, up, true);
+            if (down_b > 0) r.d2h_simplex_effective_bps = down_b / simplex(sd, down, false);
             cudaEventDestroy(go);
             cudaEventDestroy(eu);
             cudaEventDestroy(ed);
@@ -885,6 +906,41 @@ MeasuredRates Engine::calibrate() {
                                  [&](cudaStream_t s) { gemm(s, tokens, 4 * h, h); });
         r.compute_headroom = 1.05;
         r.compute_flops = 2.0 * tokens * 4.0 * h * h / sec * r.compute_headroom;  // upper bound
+    }
+    // effective compute rate: the graph's own compute tasks (up to ~0.25 s
+    // of nominal work, in task order) replayed back to back on the compute
+    // lane, each bracketed by timing events exactly as the run brackets it —
+    // per-kernel launch / event overhead and small-GEMM efficiency included
+    if (r.compute_flops > 0) {
+        compute_rate_ = r.compute_flops;
+        cudaStream_t s = lane_stream(ResourceId::gpu_compute);
+        std::vector<const Task*> replay;
+        double nominal = 0, work = 0;
+        for (const Task& t : g_.tasks) {
+            if (t.kind != TaskKind::compute || t.work <= 0.0) continue;
+            replay.push_back(&t);
+            work += t.work;
+            nominal += t.work / r.compute_flops;
+            if (nominal > 0.25) break;
+        }
+        double best = 1e30;
+        for (int it = 0; it < 2 && !replay.empty(); ++it) {
+            check_cuda(cudaDeviceSynchronize(), "sync");
+            for (const Task* t : replay) {
+                check_cuda(cudaEventRecord(events_[2 * t->id], s), "record");
+                issue_compute(*t, parse_name(t->name), s, true);
+                check_cuda(cudaEventRecord(events_[2 * t->id + 1], s), "record");
+            }
+            check_cuda(cudaDeviceSynchronize(), "compute replay");
+            double sum = 0;
+            for (const Task* t : replay) {
+                float ms = 0;
+                check_cuda(cudaEventElapsedTime(&ms, events_[2 * t->id], events_[2 * t->id + 1]), "elapsed");
+                sum += ms * 1e-3;
+            }
+            best = std::min(best, sum);
+        }
+        if (!replay.empty() && best > 0) r.compute_effective_flops = work / best;
     }
     std::size_t free_b = 0, total_b = 0;
     check_cuda(cudaMemGetInfo(&free_b, &total_b), "meminfo");
@@ -1016,6 +1072,35 @@ void Engine::wgrad(cudaStream_t s, int tokens, int in, int out, void* dst) {
     if (st != CUBLAS_STATUS_SUCCESS) throw fy::DeviceError("cublasGemmEx (wgrad) failed: status " + std::to_string(st));
 }
 
+// One compute task: the layer's real bf16 GEMMs (gemm modes; attention
+// extras as a timed spin) or a kernel that spins for work / compute_rate_.
+// replay (calibration): gradients are not written (wgrad into scratch).
+void Engine::issue_compute(const Task& t, const Parsed& p, cudaStream_t s, bool replay) {
+    const std::uint32_t k = p.block;
+    const int j = p.layer;
+    if (gemm_) {
+        int in = 0, out = 0;
+        layer_dims(j, in, out);
+        const int tokens = static_cast<int>(model_.batch_size * model_.seq_len);
+        const bool bwd = p.phase == "bwd" && p.what == "compute";
+        if (bwd) {
+            gemm(s, tokens, in, out);  // dgrad: dY[t x out] * W^T -> dX[t x in]
+            if (dataflow_ && !replay)  // wgrad straight into the block's grad buffer (the optimizer's input)
+                wgrad(s, tokens, in, out, static_cast<char*>(const_cast<void*>(d_grads_[k])) + layer_offset(j));
+            else
+                gemm(s, in, out, tokens);  // wgrad: X^T[in x t] * dY -> dW[in x out]
+        } else {
+            gemm(s, tokens, out, in);  // forward / recompute
+        }
+        // attention-score extras (extra_flops_per_block) stay timed
+        const double extra = t.work - (bwd ? 4.0 : 2.0) * double(tokens) * in * out;
+        if (extra > 1.0) spin_kernel<<<1, 32, 0, s>>>(static_cast<std::uint64_t>(extra / compute_rate_ * 1e9));
+    } else {
+        spin_kernel<<<1, 32, 0, s>>>(static_cast<std::uint64_t>(t.work / compute_rate_ * 1e9));
+    }
+    check_cuda(cudaGetLastError(), "compute launch");
+}
+
 void Engine::issue(const Task& t, ExecReport& rep) {
     cudaStream_t s = lane_stream(t.resource);
     for (const std::uint32_t d : t.deps)
@@ -1049,29 +1134,9 @@ void Engine::issue(const Task& t, ExecReport& rep) {
     const std::string& w = p.what;
     if (t.work <= 0.0) {
         // zero-byte task of the mapped graph (host tier SSD hop, HBM grads)
-    } else if (t.kind == TaskKind::compute && gemm_) {
-        int in = 0, out = 0;
-        layer_dims(j, in, out);
-        const int tokens = static_cast<int>(model_.batch_size * model_.seq_len);
-        if (p.phase == "bwd" && w == "compute") {
-            gemm(s, tokens, in, out);  // dgrad: dY[t x out] * W^T -> dX[t x in]
-            if (dataflow_)             // wgrad straight into the block's grad buffer (the optimizer's input)
-                wgrad(s, tokens, in, out, static_cast<char*>(const_cast<void*>(d_grads_[k])) + layer_offset(j));
-            else
-                gemm(s, in, out, tokens);  // wgrad: X^T[in x t] * dY -> dW[in x out]
-        } else {
-            gemm(s, tokens, out, in);  // forward / recompute
-        }
-        // attention-score extras (extra_flops_per_block) stay timed
-        const double extra = t.work - (p.phase == "bwd" && w == "compute" ? 4.0 : 2.0) *
-                                          double(tokens) * in * out;
-        if (extra > 1.0) spin_kernel<<<1, 32, 0, s>>>(static_cast<std::uint64_t>(extra / compute_rate_ * 1e9));
-        check_cuda(cudaGetLastError(), "compute launch");
     } else if (t.kind == TaskKind::compute) {
-        const double sec = t.work / compute_rate_;
-        spin_kernel<<<1, 32, 0, s>>>(static_cast<std::uint64_t>(sec * 1e9));
-        check_cuda(cudaGetLastError(), "compute launch");
-        ++rep.kernel_launches;
+        issue_compute(t, p, s, false);
+        if (!gemm_) ++rep.kernel_launches;  // cuBLAS GEMMs are not ours
     } else if (t.kind == TaskKind::optimizer_update) {
         const int slot = slot_of(k);
         fy::AdamLaunch l{};
@@ -1330,6 +1395,7 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
     if (rates.compute_flops <= 0) rates.compute_flops = hw.gpu_tput;
     rep.hw_exec = b200_hardware(hw, rates);
     rep.planned = simulate(rep.graph, rep.hw_exec);
+    link_overlap(rep.graph, rep.planned, rates);
     rep.hw_predicted = b200_hardware_effective(hw, rates);
     rep.predicted = simulate(rep.graph, rep.hw_predicted);
     rep.hw_scenario = hw;

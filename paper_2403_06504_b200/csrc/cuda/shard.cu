@@ -9,6 +9,8 @@
 
 #include "shard.cuh"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -26,7 +28,13 @@ void check_nccl(ncclResult_t r, const char* what) {
 std::uint64_t round_up(std::uint64_t x, std::uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr int kEntry = 0, kExit = 1;
-constexpr long long kBarrierTimeoutNs = 120ll * 1000 * 1000 * 1000;
+constexpr long long kBarrierTimeoutNs = 120ll * 1000 * 1000 * 1000;  // FY_BARRIER_TIMEOUT_S overrides
+
+long long barrier_timeout_ns() {
+    const char* e = std::getenv("FY_BARRIER_TIMEOUT_S");
+    const double sec = e ? std::atof(e) : 0.0;
+    return sec > 0 ? static_cast<long long>(sec * 1e9) : kBarrierTimeoutNs;
+}
 
 struct BarrierArgs {
     unsigned char* peer[kMaxWorld];  // arena base of every rank (peer mappings)
@@ -38,6 +46,7 @@ struct BarrierArgs {
     double* total;                   // sum over ranks, in rank order
     int* nonfinite_out;
     int* err;
+    long long timeout_ns;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -77,7 +86,7 @@ __global__ void shard_barrier_kernel(BarrierArgs a) {
     const long long t0 = global_ns();
     for (int r = 0; r < a.world; ++r) {
         while (ld_acquire_sys(&own->flags[a.kind][r]) < a.seq) {
-            if (global_ns() - t0 > kBarrierTimeoutNs) {
+            if (global_ns() - t0 > a.timeout_ns) {
                 *a.err = 1;  // reported by fy_shard_wait; never hang the GPU
                 return;
             }
@@ -342,6 +351,7 @@ void ShardGroup::barrier(int kind, cudaStream_t s, const double* my_norm, const 
         a.nonfinite_out = d_nonfinite_;
     }
     a.err = d_err_;
+    a.timeout_ns = barrier_timeout_ns();
     shard_barrier_kernel<<<1, 32, 0, s>>>(a);
     check_cuda(cudaGetLastError(), "barrier launch");
 }

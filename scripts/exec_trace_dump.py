@@ -29,11 +29,16 @@ if "--opts" in args:
     i = args.index("--opts")
     extra = json.loads(args[i + 1])
     del args[i:i + 2]
+suffix = ""
+if "--suffix" in args:
+    i = args.index("--suffix")
+    suffix = args[i + 1]
+    del args[i:i + 2]
 for tag in (args or list(cases)):
     sc, opts = cases[tag]
     opts = {**opts, **extra}
     st, summ, trace, err = X.execute(sc, opts, want_trace=True)
-    (out / f"exec_{tag}_summary.json").write_text(json.dumps(summ, indent=1))
-    (out / f"exec_{tag}_trace.json").write_text(trace or "")
-    (out / f"exec_{tag}_scenario.json").write_text(sc)
+    (out / f"exec_{tag}{suffix}_summary.json").write_text(json.dumps(summ, indent=1))
+    (out / f"exec_{tag}{suffix}_trace.json").write_text(trace or "")
+    (out / f"exec_{tag}{suffix}_scenario.json").write_text(sc)
     print(tag, st, err, summ["executed"]["makespan_s"], summ["planned"]["makespan_s"])
