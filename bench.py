@@ -1057,6 +1057,9 @@ def iteration_phase(F):
                     "executed_over_planned": d["executed"]["makespan_s"] / d["planned"]["makespan_s"],
                     "predicted_makespan_s": d["predicted"]["makespan_s"],
                     "executed_over_predicted": d["executed_over_predicted"],
+                    "analytic_t_iter_s": d["analytic"]["t_iter_s"],
+                    "executed_over_analytic": d["analytic"]["executed_over_analytic"],
+                    "launch": d.get("launch"),
                     "effective_link_gbs": d["hw_predicted"]["bw_gpu"] / 1e9,
                     "tasks": d["task_count"], "swap_checks": d["swap_checks"],
                     "swap_mismatches": d["swap_mismatches"],

@@ -92,6 +92,14 @@ constexpr std::uint32_t kWorkspaceFloats = 148u * 32u;
 
 // Enqueue the fused step on `stream`. Returns the CUDA launch error.
 cudaError_t launch_adamw(const AdamLaunch& a, cudaStream_t stream);
+
+// Loads every kernel of the modules that contain `anchors` (plus this
+// file's update kernels) on the CURRENT device. Under CUDA lazy loading
+// (the CUDA 12 default) a kernel's first launch loads it, and loading may
+// wait for the device to go idle — behind a device barrier that spins until
+// a peer's kernel runs, that first launch deadlocks (fy_shard: W shards in
+// one fresh process). Idempotent; cheap after the first call per device.
+cudaError_t preload_kernels(const void* const* anchors, int count);
 // The same step for a list of chunks in ONE persistent TMA launch per
 // kMaxChunksPerLaunch chunks (concatenated tile space; grad_sq_sum = the sum
 // over the list, taken from list[0] like dtypes, scalars and outputs). Falls

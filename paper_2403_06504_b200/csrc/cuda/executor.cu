@@ -354,7 +354,13 @@ private:
         check_cuda(capturing_ ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s),
                    "record");
     }
-    cudaEvent_t end_dep(std::uint32_t id) const { return capturing_ ? deps_[id] : events_[2 * id + 1]; }
+    // what a dependent task waits on: zero-work tasks issue no GPU work and
+    // no timing event, only their dependency point (deps_); in a capture a
+    // plain record is an edge, not a node
+    cudaEvent_t end_dep(std::uint32_t id) const {
+        return capturing_ || g_.tasks[id].work <= 0.0 ? deps_[id] : events_[2 * id + 1];
+    }
+    std::vector<std::uint32_t> issued_;  // issue order (each lane's FIFO order)
     bool run_graph(const std::vector<std::pair<std::uint64_t, std::uint32_t>>& order, ExecReport& rep);
 
     // host side
@@ -1129,11 +1135,21 @@ void Engine::issue(const Task& t, ExecReport& rep) {
         phys(write ? "file_write" : "file_read", bytes);
     };
 
-    record_time(events_[2 * t.id], s);
+    // Instrumentation is one timing event per task, at its END: a task
+    // starts when its lane's previous task and its dependencies are done, so
+    // its start is reconstructed from those ends after the run (run()). A
+    // start event-record node per task cost ~5-9 us of device latency on
+    // every edge of the critical path (r02f: C1 with HBM-resident states
+    // spent ~19 us per compute task in them).
+    issued_.push_back(t.id);
     const std::uint64_t state_b = 12 * n_, param_b = 2 * n_;
     const std::string& w = p.what;
     if (t.work <= 0.0) {
-        // zero-byte task of the mapped graph (host tier SSD hop, HBM grads)
+        // zero-byte task of the mapped graph (host tier SSD hop, HBM grads):
+        // its dependencies are waited on above (the lane stays FIFO behind
+        // them) and its end is a dependency point only — no GPU node
+        check_cuda(cudaEventRecord(deps_[t.id], s), "record dep");
+        return;
     } else if (t.kind == TaskKind::compute) {
         issue_compute(t, p, s, false);
         if (!gemm_) ++rep.kernel_launches;  // cuBLAS GEMMs are not ours
@@ -1258,6 +1274,7 @@ bool Engine::run_graph(const std::vector<std::pair<std::uint64_t, std::uint32_t>
             throw;
         }
         rep = saved;  // the stream-mode issue starts from a clean report
+        issued_.clear();
         io_reqs_.resize(io_mark);
         wscratch_turn_ = turn;
     }
@@ -1276,6 +1293,7 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
     std::sort(order.begin(), order.end());
 
     check_cuda(cudaDeviceSynchronize(), "pre-run sync");
+    issued_.clear();
     rep.launch_mode = "stream";
     if (opt_.launch == "graph" && run_graph(order, rep)) {
         rep.launch_mode = "graph";
@@ -1318,18 +1336,32 @@ void Engine::run(const SimTrace& planned, ExecReport& rep) {
     if (opt_.checksum_states && has_update_) rep.state_checksum = checksum_states();
     check_cuda(cudaMemcpy(&rep.nonfinite, d_bad_.p, sizeof(int), cudaMemcpyDeviceToHost), "flag");
 
-    // real trace from the events
+    // real trace: measured ends (timing events); each start = the later of
+    // its lane predecessor's end and its dependencies' ends (when the stream
+    // let the operation begin); zero-work tasks take no time
     SimTrace& tr = rep.trace;
     tr.header = g_.header;
     tr.events.clear();
+    std::vector<std::uint64_t> end_ns(g_.tasks.size(), 0);
+    std::map<ResourceId, std::uint64_t> lane_end;
+    std::vector<TraceEvent> evs(g_.tasks.size());
+    for (const std::uint32_t id : issued_) {
+        const Task& t = g_.tasks[id];
+        std::uint64_t start = lane_end[t.resource];
+        for (const std::uint32_t d : t.deps) start = std::max(start, end_ns[d]);
+        std::uint64_t end = start;
+        if (t.work > 0.0) {
+            float ms1 = 0;
+            check_cuda(cudaEventElapsedTime(&ms1, base_, events_[2 * t.id + 1]), "elapsed");
+            end = static_cast<std::uint64_t>(std::llround(std::max(0.0f, ms1) * 1e6));
+            if (end < start) start = end;  // timer jitter: never a negative duration
+        }
+        end_ns[id] = end;
+        lane_end[t.resource] = end;
+        evs[id] = TraceEvent{t.id, t.resource, t.dir, t.payload, t.work, start, end};
+    }
     for (const Task& t : g_.tasks) {
-        float ms0 = 0, ms1 = 0;
-        check_cuda(cudaEventElapsedTime(&ms0, base_, events_[2 * t.id]), "elapsed");
-        check_cuda(cudaEventElapsedTime(&ms1, base_, events_[2 * t.id + 1]), "elapsed");
-        TraceEvent e{t.id, t.resource, t.dir, t.payload, t.work,
-                     static_cast<std::uint64_t>(std::llround(std::max(0.0f, ms0) * 1e6)),
-                     static_cast<std::uint64_t>(std::llround(std::max(0.0f, ms1) * 1e6))};
-        if (e.end_ns < e.start_ns) e.end_ns = e.start_ns;
+        const TraceEvent& e = evs[t.id];
         tr.events.push_back(e);
         tr.makespan_ns = std::max(tr.makespan_ns, e.end_ns);
         tr.busy_ns[t.resource] += e.end_ns - e.start_ns;

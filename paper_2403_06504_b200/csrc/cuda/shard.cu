@@ -168,6 +168,10 @@ ShardGroup::ShardGroup(const fy_shard_config& cfg) : cfg_(cfg) {
         upd_t1_.resize(cfg_.chunk_count);
         for (cudaEvent_t& e : upd_t0_) check_cuda(cudaEventCreate(&e), "event");
         for (cudaEvent_t& e : upd_t1_) check_cuda(cudaEventCreate(&e), "event");
+        // every kernel a step may launch is loaded now, before any device
+        // barrier can spin (lazy loading would deadlock behind it)
+        const void* anchors[] = {reinterpret_cast<const void*>(shard_barrier_kernel)};
+        check_cuda(preload_kernels(anchors, 1), "preload kernels");
         check_cuda(cudaMalloc(&workspace_, sizeof(float) * kWorkspaceFloats), "workspace");
         check_cuda(cudaMalloc(&d_norm_, sizeof(double)), "norm");
         check_cuda(cudaMalloc(&d_total_, sizeof(double)), "norm");

@@ -12,7 +12,8 @@ scenario schema, no new keys).
                 replayed one direction at a time (H2D, the binding lane of
                 every measured iteration); per workload
   cpu_opt_tput  the fused Adam kernel (params/s, HBM-resident states)
-  gpu_tput      bf16 cuBLAS GEMM FLOP/s of the model's largest layer GEMM
+  gpu_tput      bf16 cuBLAS FLOP/s of the model's own layer GEMMs replayed
+                back to back (compute_effective_flops)
   bw_s2c/bw_c2s the file tier (O_DIRECT io_uring) when measured, else the
                 preset's SSD array is kept
   gpu_mem/cpu_mem this box
@@ -49,7 +50,7 @@ f = rates.get("13b_file", {})
 hw = {"preset": "a100-12ssd", "name": "b200-measured",
       "bw_gpu": big["h2d_simplex_effective_bps"],
       "cpu_opt_tput": big["optimizer_params_per_s"],
-      "gpu_tput": big["compute_flops"],
+      "gpu_tput": big.get("compute_effective_flops") or big["compute_flops"],
       "gpu_mem": 180000000000}
 if f.get("file_read_effective_bps"):
     hw.update(n_ssd=1, bw_s2c=f["file_read_effective_bps"], bw_c2s=f["file_write_effective_bps"])

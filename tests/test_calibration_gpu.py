@@ -1,0 +1,97 @@
+"""GPU: the calibration loop of SURVEY §8(f)-3 held to the reference's
+acceptance bar (proj/tests/acceptance/acceptance_main.cpp:345-364: max error
+<= 15%, median <= 8%).
+
+The reference checks its analytic t_iter (proj/src/cost_model.cpp:70-90)
+against its DES. Here both models are checked against EXECUTED iterations
+on the B200 (offsim_execute: every task of the planner's graph on real
+engines) for C1 (GPT-2-small shape) at b=8 and b=128, C1 with every
+optimizer group resident in HBM, and a 4-block slice of the 13B shape with
+real bf16 GEMMs feeding the optimizer (host tier and HBM-resident):
+
+* the DES (the unchanged simulate()) on the in-run calibrated effective
+  rates — duplex-aware link replays, the graph's own compute replayed —
+  must predict the executed makespan within the acceptance bar;
+* the persisted `b200-measured` preset (paper_2403_06504_b200/presets,
+  written by scripts/calibrate_b200.py) as the scenario's hardware: the DES
+  on it must predict the large-copy 13B-shape iterations within 15%;
+* the analytic model's structure (per phase, the busiest lane) on the same
+  rates is reported beside it; it ignores pipeline fill / drain and
+  dependency latency (the reference only holds it to the bar in its
+  8..96-block stratum, against its own DES): here it gets a sanity bound."""
+import json
+import statistics
+from pathlib import Path
+
+import pytest
+
+from exec_api import execute, scenario
+
+pytestmark = pytest.mark.gpu
+
+RATE = 1.4e15
+PRESET = Path(__file__).resolve().parents[1] / "paper_2403_06504_b200" / "presets" / "b200_measured.json"
+C13 = dict(layers=4, heads=40, hidden=5120, batch=8, name="13b4")
+CASES = {
+    "c1_b8": (scenario(batch=8), {"tier": "host", "compute_rate": RATE}),
+    "c1_b8_resident": (scenario(batch=8), {"tier": "host", "compute_rate": RATE, "resident_groups": "all"}),
+    "c1_b128": (scenario(batch=128), {"tier": "host", "compute_rate": RATE}),
+    "13b_4blk": (scenario(**C13), {"tier": "host", "compute_mode": "gemm_dataflow"}),
+    "13b_4blk_resident": (scenario(**C13), {"tier": "host", "compute_mode": "gemm_dataflow",
+                                            "resident_groups": "all"}),
+}
+
+
+@pytest.fixture(scope="module")
+def runs(cuda_dev):
+    out = {}
+    for tag, (sc, opts) in CASES.items():
+        st, s, _, err = execute(sc, opts)
+        assert st == 0, (tag, err)
+        assert s["all_invariants_pass"], tag
+        out[tag] = s
+    return out
+
+
+def _errs(runs, model):
+    errs = {}
+    for tag, s in runs.items():
+        ex = s["executed"]["makespan_s"]
+        pred = s["predicted"]["makespan_s"] if model == "des" else s["analytic"]["t_iter_s"]
+        errs[tag] = abs(pred - ex) / ex
+    return errs
+
+
+def test_des_prediction_within_acceptance_bar(runs):
+    errs = _errs(runs, "des")
+    print(json.dumps({k: round(v, 4) for k, v in errs.items()}))
+    assert max(errs.values()) <= 0.15, errs
+    assert statistics.median(errs.values()) <= 0.08, errs
+
+
+def test_analytic_model_reported_and_bounded(runs):
+    """The analytic structure (per phase, the busiest lane; no fill / drain,
+    no dependency latency) is a coarse model: r02g measured 15-27% error on
+    C1 and 33-41% on the 4-block 13B slice (fill / drain is half the slice).
+    It is reported (bench `executed_iteration`), not used for decisions on
+    B200, and held only to a sanity bound here."""
+    errs = _errs(runs, "analytic")
+    print(json.dumps({k: round(v, 4) for k, v in errs.items()}))
+    c1 = {k: v for k, v in errs.items() if k.startswith("c1")}
+    assert max(c1.values()) <= 0.35, c1
+    assert max(errs.values()) <= 0.6, errs
+
+
+def test_persisted_preset_predicts_large_copy_iterations(cuda_dev):
+    if not PRESET.exists():
+        pytest.skip("no persisted preset (run scripts/calibrate_b200.py on a B200)")
+    hw = json.loads(PRESET.read_text())["hardware"]
+    for tag in ("13b_4blk", "13b_4blk_resident"):
+        sc, opts = CASES[tag]
+        doc = json.loads(sc)
+        doc["hardware"] = hw
+        st, s, _, err = execute(json.dumps(doc), opts)
+        assert st == 0, err
+        sp = s["scenario_prediction"]
+        assert sp["hardware"] == "b200-measured"
+        assert abs(sp["executed_over_des"] - 1.0) <= 0.15, (tag, sp)
