@@ -786,7 +786,7 @@ def streamed_shard_phase(torch, F, args, world, rank, local):
     (fy_shard_*, FY_TIER_HOST): GPT-3-175B-shaped blocks (1,811,939,328
     params) whose master/m/v live in each rank's NUMA-local pinned host
     memory (fy_host_alloc). Every block is sharded across the ranks; each
-    rank streams its slice through the library's chunk pipeline as 4 strided
+    rank streams its slice through the library's chunk pipeline as 16 strided
     pieces (12 B/param H2D, 12 B/param states + 2 B/param bf16 params D2H,
     grads in HBM) and the block's NCCL all-gather of the updated bf16 params
     runs on the shard's comm stream as soon as the block is updated,
@@ -798,7 +798,7 @@ def streamed_shard_phase(torch, F, args, world, rank, local):
     links = link_probe(torch, world, rank)
     dev = torch.device("cuda", local)
     sizes = [N4] * K
-    pieces = 4
+    pieces = 16  # fill / drain = one piece each way: ~2% of the step at 16 pieces, ~10% at 4
     probe = F.optim.shard_range(N4, world, rank, 8)[1]
     piece = max(8, (-(-probe // pieces) + 7) // 8 * 8)
     sh, gather, note = make_shard(torch, F, args, world, rank, local, sizes, "host", "nccl",

@@ -180,6 +180,8 @@ struct MeasuredRates {
     // back to back on both lanes at once (duplex, real copy sizes): what an
     // overlapped schedule actually gets from PCIe, vs the simplex burst
     // rates above.
+    // the graph's own copies of one direction while the other direction is
+    // continuously busy (duplex contention)
     double h2d_effective_bps = 0.0;
     double d2h_effective_bps = 0.0;
     // the same copies replayed one direction at a time (per-copy overhead,

@@ -728,9 +728,10 @@ MeasuredRates Engine::calibrate() {
     r.d2h_bps = bytes / timed(lane_stream(ResourceId::link_g2c), [&](cudaStream_t s) {
                     check_cuda(cudaMemcpyAsync(h.p, slot, bytes, cudaMemcpyDeviceToHost, s), "d2h");
                 });
-    // Effective duplex rates: replay this graph's own copy sizes (capped at
-    // 256 MiB each, 2 GiB per direction, in task order) back to back on both
-    // link lanes at once — small copies and duplex contention included.
+    // Effective link rates: replay this graph's own copy sizes (capped at
+    // 256 MiB each, 2 GiB per direction, in task order) per direction, under
+    // continuous load from the other direction and alone — small copies and
+    // duplex contention included; tier_map blends the two per lane.
     {
         constexpr std::uint64_t kEach = 256ull << 20, kTotal = 2ull << 30;
         std::vector<std::uint64_t> up, down;
@@ -751,26 +752,44 @@ MeasuredRates Engine::calibrate() {
             check_cuda(cudaEventCreate(&go), "event");
             check_cuda(cudaEventCreate(&eu), "event");
             check_cuda(cudaEventCreate(&ed), "event");
-            double best_u = 1e30, best_d = 1e30;
-            for (int it = 0; it < 2; ++it) {
-                check_cuda(cudaDeviceSynchronize(), "sync");
-                check_cuda(cudaEventRecord(go, su), "record");
-                check_cuda(cudaStreamWaitEvent(sd, go, 0), "wait");
-                for (const std::uint64_t b : up)
-                    check_cuda(cudaMemcpyAsync(du.p, hu.p, b, cudaMemcpyHostToDevice, su), "h2d");
-                for (const std::uint64_t b : down)
-                    check_cuda(cudaMemcpyAsync(hd.p, dd.p, b, cudaMemcpyDeviceToHost, sd), "d2h");
-                check_cuda(cudaEventRecord(eu, su), "record");
-                check_cuda(cudaEventRecord(ed, sd), "record");
-                check_cuda(cudaDeviceSynchronize(), "sync");
-                float mu = 0, md = 0;
-                check_cuda(cudaEventElapsedTime(&mu, go, eu), "elapsed");
-                check_cuda(cudaEventElapsedTime(&md, go, ed), "elapsed");
-                best_u = std::min(best_u, mu * 1e-3);
-                best_d = std::min(best_d, md * 1e-3);
-            }
-            if (up_b > 0) r.h2d_effective_bps = up_b / best_u;
-            if (down_b > 0) r.d2h_effective_bps = down_b / best_d;
+            // each direction's own copies while the OTHER direction is busy
+            // the whole time (its copies looped past the measured
+            // direction's end): the rate a copy gets when both directions
+            // run — small H2D copies under a D2H lose much more than the
+            // 1 GiB duplex probe suggests (r02g: a 1.2 MB H2D at 11 GB/s
+            // beside a 6 MB D2H)
+            auto loaded = [&](cudaStream_t sm, const std::vector<std::uint64_t>& main_sizes, std::uint64_t main_b,
+                              bool main_h2d, cudaStream_t so, const std::vector<std::uint64_t>& other_sizes,
+                              std::uint64_t other_b) {
+                if (main_sizes.empty()) return 0.0;
+                if (other_sizes.empty()) return -1.0;  // nothing to contend with
+                const int reps = static_cast<int>(std::min<std::uint64_t>(
+                    16, 1 + (main_b * 3 / 2 + other_b - 1) / std::max<std::uint64_t>(other_b, 1)));
+                double best = 1e30;
+                for (int it = 0; it < 2; ++it) {
+                    check_cuda(cudaDeviceSynchronize(), "sync");
+                    check_cuda(cudaEventRecord(go, so), "record");
+                    for (int k = 0; k < reps; ++k)
+                        for (const std::uint64_t b : other_sizes)
+                            check_cuda(main_h2d ? cudaMemcpyAsync(hd.p, dd.p, b, cudaMemcpyDeviceToHost, so)
+                                                : cudaMemcpyAsync(du.p, hu.p, b, cudaMemcpyHostToDevice, so),
+                                       "load replay");
+                    check_cuda(cudaStreamWaitEvent(sm, go, 0), "wait");
+                    check_cuda(cudaEventRecord(ed, sm), "record");
+                    for (const std::uint64_t b : main_sizes)
+                        check_cuda(main_h2d ? cudaMemcpyAsync(du.p, hu.p, b, cudaMemcpyHostToDevice, sm)
+                                            : cudaMemcpyAsync(hd.p, dd.p, b, cudaMemcpyDeviceToHost, sm),
+                                   "loaded replay");
+                    check_cuda(cudaEventRecord(eu, sm), "record");
+                    check_cuda(cudaDeviceSynchronize(), "sync");
+                    float ms = 0;
+                    check_cuda(cudaEventElapsedTime(&ms, ed, eu), "elapsed");
+                    best = std::min(best, ms * 1e-3);
+                }
+                return main_b / best;
+            };
+            const double up_loaded = loaded(su, up, up_b, true, sd, down, down_b);
+            const double down_loaded = loaded(sd, down, down_b, false, su, up, up_b);
             // the same copies one direction at a time
             auto simplex = [&](cudaStream_t st, const std::vector<std::uint64_t>& sizes, bool h2d) {
                 double best = 1e30;
@@ -791,6 +810,9 @@ MeasuredRates Engine::calibrate() {
             };
             if (up_b > 0) r.h2d_simplex_effective_bps = up_b / simplex(su, up, true);
             if (down_b > 0) r.d2h_simplex_effective_bps = down_b / simplex(sd, down, false);
+            // no copies the other way: the loaded rate is the simplex one
+            r.h2d_effective_bps = up_loaded < 0 ? r.h2d_simplex_effective_bps : up_loaded;
+            r.d2h_effective_bps = down_loaded < 0 ? r.d2h_simplex_effective_bps : down_loaded;
             cudaEventDestroy(go);
             cudaEventDestroy(eu);
             cudaEventDestroy(ed);
