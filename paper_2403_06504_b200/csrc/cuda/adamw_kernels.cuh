@@ -137,7 +137,7 @@ void set_max_ctas(int max_ctas);
 // Stages / consumer warps the TMA path runs on a device with `sms` SMs under
 // the current budget / tuning.
 int tma_stages(int sms);
-int tma_consumer_warps(int sms);
+int tma_consumer_warps(int sms, bool fp32_grads = false);
 #ifdef FY_SWEEP_VARIANTS
 // Sweep build only (build/sweep): TMA variants for bf16 -> bf16: elements
 // per stage (1024 | 2048 | 4096), separate load / store DMA warps; probe

@@ -587,7 +587,7 @@ void ShardGroup::stats(fy_shard_stats* out) const {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg_.device);
     out->stages = tma_stages(sms > 0 ? sms : 148);
-    out->consumer_warps = tma_consumer_warps(sms > 0 ? sms : 148);
+    out->consumer_warps = tma_consumer_warps(sms > 0 ? sms : 148, cfg_.grad_dtype == FY_FP32);
 }
 
 } // namespace fy
