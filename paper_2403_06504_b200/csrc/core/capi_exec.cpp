@@ -304,8 +304,10 @@ SwapPlan plan_with_placement(const Scenario& s, const std::string& placement) {
     return plan_swaps(s.model, s.hardware, o);
 }
 
-// Dry run: the mapped graph and its DES on nominal B200 rates (no GPU).
-std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVariant v) {
+// Dry run: the mapped graph and its DES on nominal B200 rates (no GPU);
+// trace_out (optional) receives that DES trace as a Chrome trace.
+std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVariant v,
+                         std::string* trace_out = nullptr) {
     const SwapPlan plan = plan_with_placement(s, po.placement);
     const TaskGraph ref = build_schedule(s.model, s.hardware, plan, v);
     TaskGraph mapped = map_graph_for_b200(ref, po.exec.tier, po.exec.state_slots,
@@ -323,6 +325,9 @@ std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVar
     const HardwareConfig hw = b200_hardware(s.hardware, nominal);
     const SimTrace tr = simulate(mapped, hw);
     const InvariantReport inv = check_trace_invariants(mapped, tr, hw);
+    if (trace_out) *trace_out = to_chrome_trace_json(mapped, tr);
+    MeasuredRates overlap;
+    link_overlap(mapped, tr, overlap);
     std::map<std::string, double> ref_bytes, mapped_bytes;
     for (const Task& t : ref.tasks)
         if (t.kind == TaskKind::transfer)
@@ -351,6 +356,11 @@ std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVar
                       {"reference_bytes", bytes_json(ref_bytes)},
                       {"mapped_bytes", bytes_json(mapped_bytes)},
                       {"planned", trace_stats(tr)},
+                      {"analytic", analytic_json(mapped, hw, tr.makespan_s())},
+                      {"link_overlap", json{{"c2g", overlap.c2g_overlap},
+                                            {"g2c", overlap.g2c_overlap},
+                                            {"c2g_bytes", overlap.c2g_bytes},
+                                            {"g2c_bytes", overlap.g2c_bytes}}},
                       {"invariants", checks},
                       {"all_invariants_pass", inv.all_pass}};
     return doc.dump(2) + "\n";
@@ -365,8 +375,9 @@ offsim_status run_exec(const Scenario& s, const char* opts_json,
     Scenario sv = s;
     sv.variant = v;
     if (po.dry_run) {
-        *summary_out = capi::copy_out(dry_run_json(sv, po, v));
-        if (trace_out) *trace_out = nullptr;
+        std::string trace;
+        *summary_out = capi::copy_out(dry_run_json(sv, po, v, trace_out ? &trace : nullptr));
+        if (trace_out) *trace_out = capi::copy_out(trace);
         return OFFSIM_OK;
     }
     const SwapPlan plan = plan_with_placement(sv, po.placement);

@@ -164,3 +164,56 @@ def test_io_depth_option():
     for bad in (0, 2000):
         st, _, _, err = execute(C1, {"dry_run": True, "tier": "file", "io_depth": bad})
         assert st == 2 and "io_depth" in err
+
+
+def _dry_trace(sc, opts):
+    import json
+    st, s, tr, err = execute(sc, {"dry_run": True, **opts}, want_trace=True)
+    assert st == 0, err
+    d = json.loads(tr)
+    lanes = {e["tid"]: e["args"]["name"] for e in d["traceEvents"] if e.get("ph") == "M"
+             and e["name"] == "thread_name"}
+    ev = [(lanes[e["tid"]], e["name"], e["ts"], e["dur"]) for e in d["traceEvents"] if e.get("ph") == "X"]
+    return s, ev
+
+
+@pytest.mark.parametrize("sc,opts", [(C1, {"tier": "host"}), (C1, {"tier": "host", "resident_groups": "all"}),
+                                     (C2, {"tier": "host"})])
+def test_analytic_model_is_per_phase_busiest_lane(sc, opts):
+    """analytic_iteration (the reference cost model's structure on the mapped
+    graph, cost_model.cpp:26-90): t_f / t_bo = the busiest lane's summed
+    task durations over the forward tasks / the backward + optimizer tasks;
+    recomputed here from the DES trace's own durations."""
+    from collections import defaultdict
+    s, ev = _dry_trace(sc, opts)
+    phase = {"fwd": defaultdict(float), "rest": defaultdict(float)}
+    for lane, name, ts, dur in ev:
+        phase["fwd" if name.startswith("fwd ") else "rest"][lane] += dur * 1e-6
+    a = s["analytic"]
+    assert a["t_f_s"] == pytest.approx(max(phase["fwd"].values()), rel=1e-6)
+    assert a["t_bo_s"] == pytest.approx(max(phase["rest"].values()), rel=1e-6)
+    assert a["t_iter_s"] == pytest.approx(a["t_f_s"] + a["t_bo_s"], rel=1e-12)
+    assert a["t_iter_s"] <= s["planned"]["makespan_s"] * 2.0
+
+
+@pytest.mark.parametrize("sc,opts", [(C1, {"tier": "host"}), (C1, {"tier": "host", "resident_groups": "all"}),
+                                     (C2, {"tier": "host"})])
+def test_link_overlap_matches_trace(sc, opts):
+    """link_overlap: the share of each link lane's busy time during which the
+    other direction is busy (the weight of the duplex-loaded replay in the
+    effective link rate), recomputed from the DES trace's intervals."""
+    s, ev = _dry_trace(sc, opts)
+    up = sorted((ts, ts + dur) for lane, _, ts, dur in ev if lane == "CPU to GPU" and dur > 0)
+    down = sorted((ts, ts + dur) for lane, _, ts, dur in ev if lane == "GPU to CPU" and dur > 0)
+    both, i, j = 0.0, 0, 0
+    while i < len(up) and j < len(down):
+        lo, hi = max(up[i][0], down[j][0]), min(up[i][1], down[j][1])
+        both += max(0.0, hi - lo)
+        if up[i][1] < down[j][1]:
+            i += 1
+        else:
+            j += 1
+    lo = s["link_overlap"]
+    assert lo["c2g"] == pytest.approx(both / sum(b - a for a, b in up), abs=1e-6)
+    assert lo["g2c"] == pytest.approx(both / sum(b - a for a, b in down), abs=1e-6)
+    assert 0.0 <= lo["c2g"] <= 1.0 and 0.0 <= lo["g2c"] <= 1.0
