@@ -98,6 +98,8 @@ def parse():
     ap.add_argument("--shard-blocks", type=int, default=2,
                     help="175B-shaped blocks per step in the streamed-shard phase (0 = skip)")
     ap.add_argument("--no-backward-overlap", action="store_true")
+    ap.add_argument("--no-iteration", action="store_true",
+                    help="skip the executed-iteration phase (e.g. for an ncu launch list of the headline)")
     ap.add_argument("--gather", choices=["auto", "nccl", "peer", "fused"], default="auto",
                     help="N>1 (fy_shard gather): the kernel's fused peer-store epilogue into the "
                          "peers' IPC-mapped arenas (NVLink; 'peer' = 'fused'), or an in-place NCCL "
@@ -1376,7 +1378,8 @@ def main():
 
     if rank == 0 and world == 1:
         try:
-            extra["executed_iteration"] = iteration_phase(F)
+            if not args.no_iteration:
+                extra["executed_iteration"] = iteration_phase(F)
         except Exception as e:  # evidence only; never masks the headline
             extra["executed_iteration"] = f"failed: {e}"
         if args.ssd_tier:
@@ -1432,7 +1435,7 @@ def main():
             "parallelism": (f"shard{world}" if world > 1 else "single")
                            + (f"+{res['gather']}-gather" if res.get("gather") else ""),
             "gather_note": res.get("gather_note"),
-            "l2": "inputs larger than L2 (176 GB resident)",
+            "l2": f"inputs larger than L2 ({14 * P / 1e9:.0f} GB resident, L2 126 MB)",
             "hparams": "lr 1e-4, betas (0.9, 0.95), eps 1e-8, wd 0.1, adamw, bias corr",
             "gb_per_s_at_28B": res["value"] * BYTES_RESIDENT / 1e9,
         },
