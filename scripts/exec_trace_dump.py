@@ -19,6 +19,9 @@ cases = {
                  {"tier": "host", "compute_mode": "gemm"}),
     "c1_b8_resident": (X.scenario(batch=8), {"tier": "host", "compute_rate": 1.4e15,
                                              "resident_groups": "all"}),
+    "c1_b8_file": (X.scenario(batch=8), {"tier": "file", "file_dir": "/tmp/offsim_dump_file", "compute_rate": 1.4e15}),
+    "13b_2blk_file": (X.scenario(layers=2, heads=40, hidden=5120, batch=8, name="13b2"),
+                      {"tier": "file", "file_dir": "/tmp/offsim_dump_file", "compute_mode": "gemm"}),
     "13b_4blk_resident": (X.scenario(layers=4, heads=40, hidden=5120, batch=8, name="13b4"),
                           {"tier": "host", "compute_mode": "gemm_dataflow", "resident_groups": "all"}),
 }
