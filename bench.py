@@ -1118,7 +1118,7 @@ def swap_engine_phase(torch, F, blocks_cpu=40, blocks_ssd=8):
     return out
 
 
-def swap_sweep_phase(F, budget_cpu=32e9, budget_ssd=8e9):
+def swap_sweep_phase(F, budget_cpu=32e9, budget_ssd=16e9):
     """BASELINE config 5: activation swap GPU->host(->SSD) bandwidth sweep,
     13B shape, s=2048, b in {8,16,32,64}, swap amounts chosen by the
     unchanged planner (a100 preset; coefficients 0/0/1/1, checkpoints on

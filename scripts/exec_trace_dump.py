@@ -8,23 +8,12 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
+sys.path.insert(0, str(ROOT / "scripts"))
 import exec_api as X  # noqa: E402
 
 out = ROOT / "gpurun_out"
 out.mkdir(exist_ok=True)
-cases = {
-    "c1_b8": (X.scenario(batch=8), {"tier": "host", "compute_rate": 1.4e15}),
-    "c1_b128": (X.scenario(batch=128), {"tier": "host", "compute_rate": 1.4e15}),
-    "13b_4blk": (X.scenario(layers=4, heads=40, hidden=5120, batch=8, name="13b4"),
-                 {"tier": "host", "compute_mode": "gemm"}),
-    "c1_b8_resident": (X.scenario(batch=8), {"tier": "host", "compute_rate": 1.4e15,
-                                             "resident_groups": "all"}),
-    "c1_b8_file": (X.scenario(batch=8), {"tier": "file", "file_dir": "/tmp/offsim_dump_file", "compute_rate": 1.4e15}),
-    "13b_2blk_file": (X.scenario(layers=2, heads=40, hidden=5120, batch=8, name="13b2"),
-                      {"tier": "file", "file_dir": "/tmp/offsim_dump_file", "compute_mode": "gemm"}),
-    "13b_4blk_resident": (X.scenario(layers=4, heads=40, hidden=5120, batch=8, name="13b4"),
-                          {"tier": "host", "compute_mode": "gemm_dataflow", "resident_groups": "all"}),
-}
+from exec_cases import CASES as cases  # noqa: E402
 # args: [tag ...] [--opts JSON] (extra ExecOptions merged into every case)
 args = sys.argv[1:]
 extra = {}

@@ -7,7 +7,9 @@ against its DES. Here both models are checked against EXECUTED iterations
 on the B200 (offsim_execute: every task of the planner's graph on real
 engines) for C1 (GPT-2-small shape) at b=8 and b=128, C1 with every
 optimizer group resident in HBM, and a 4-block slice of the 13B shape with
-real bf16 GEMMs feeding the optimizer (host tier and HBM-resident):
+real bf16 GEMMs feeding the optimizer (host tier and HBM-resident), and a
+wider matrix (C1 b=32/64, 8-block 13B slices at b=8/32, a 4-block 65B slice
+with resident states) — ten iterations:
 
 * the DES (the unchanged simulate()) on the in-run calibrated effective
   rates — duplex-aware link replays, the graph's own compute replayed —
@@ -39,6 +41,15 @@ CASES = {
     "13b_4blk": (scenario(**C13), {"tier": "host", "compute_mode": "gemm_dataflow"}),
     "13b_4blk_resident": (scenario(**C13), {"tier": "host", "compute_mode": "gemm_dataflow",
                                             "resident_groups": "all"}),
+    # the wider matrix (r02r): more batches, longer slices, a 65B slice
+    "c1_b32": (scenario(batch=32), {"tier": "host", "compute_rate": RATE}),
+    "c1_b64": (scenario(batch=64), {"tier": "host", "compute_rate": RATE}),
+    "13b_8blk": (scenario(layers=8, heads=40, hidden=5120, batch=8, name="13b8"),
+                 {"tier": "host", "compute_mode": "gemm_dataflow"}),
+    "13b_8blk_b32": (scenario(layers=8, heads=40, hidden=5120, batch=32, name="13b8"),
+                     {"tier": "host", "compute_mode": "gemm_dataflow"}),
+    "65b_4blk_resident": (scenario(layers=4, heads=64, hidden=8192, batch=8, name="65b4"),
+                          {"tier": "host", "compute_mode": "gemm_dataflow", "resident_groups": "all"}),
 }
 
 
@@ -86,7 +97,7 @@ def test_persisted_preset_predicts_large_copy_iterations(cuda_dev):
     if not PRESET.exists():
         pytest.skip("no persisted preset (run scripts/calibrate_b200.py on a B200)")
     hw = json.loads(PRESET.read_text())["hardware"]
-    for tag in ("13b_4blk", "13b_4blk_resident"):
+    for tag in ("13b_4blk", "13b_4blk_resident", "13b_8blk"):
         sc, opts = CASES[tag]
         doc = json.loads(sc)
         doc["hardware"] = hw
