@@ -239,8 +239,16 @@ fy_status fy_shard_range(uint64_t n, uint32_t world, uint32_t rank, uint32_t ali
  * rank's barrier spins: one process per GPU always has that; a process that
  * drives several shards on ONE device must keep its streams (3 per shard)
  * within CUDA_DEVICE_MAX_CONNECTIONS (default 8; streams beyond it share
- * hardware queues and serialise). A barrier that waits > 120 s gives up and
+ * hardware queues and serialise: 8 shards on one device need 32). Every
+ * kernel a step may launch is loaded at fy_shard_create (under CUDA's lazy
+ * loading a first launch behind a spinning barrier would deadlock). A
+ * barrier that waits > 120 s (env FY_BARRIER_TIMEOUT_S) gives up and
  * fy_shard_wait reports FY_ERR_DEVICE instead of hanging the GPU.
+ * In-place gradients: io.grad may point at this rank's own slot of the
+ * chunk's arena region (fy_shard_slice.params + rank * stride elements,
+ * 16-bit grads): the update then overwrites the gradients with the params,
+ * the reference's convention (proj/src/task_graph.cpp:493-495), and the
+ * caller needs no separate gradient memory.
  * want_grad_norm: the GLOBAL sum of squares over all ranks (one 8-byte
  * all-reduce, or the exit barrier's exchange summed in rank order).
  * Step counter: one DeepSpeed IncrementStep per chunk (fy_adam_counter
