@@ -586,7 +586,8 @@ void ShardGroup::stats(fy_shard_stats* out) const {
     out->gather = cfg_.gather;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg_.device);
-    out->stages = tma_stages(sms > 0 ? sms : 148);
+    const int n_sms = sms > 0 ? sms : 148;
+    out->stages = cfg_.grad_dtype != FY_FP32 && budgeted_split(n_sms) ? 6 : tma_stages(n_sms);
     out->consumer_warps = tma_consumer_warps(sms > 0 ? sms : 148, cfg_.grad_dtype == FY_FP32);
 }
 
