@@ -138,7 +138,7 @@ void set_max_ctas(int max_ctas);
 // the current budget / tuning.
 int tma_stages(int sms);
 int tma_consumer_warps(int sms, bool fp32_grads = false);
-// SM budget of >= 48 CTAs with the automatic shape: 16-bit-gradient launches
+// SM budget of 48..112 CTAs with the automatic shape: 16-bit-gradient launches
 // run separate load / store DMA warps and 6 stages.
 bool budgeted_split(int sms);
 #ifdef FY_SWEEP_VARIANTS
