@@ -92,7 +92,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streamed-chunks", type=int, default=6)
     ap.add_argument("--streamed-pieces", type=int, default=4)
-    ap.add_argument("--cpu-sample-chunks", type=int, default=2)
+    ap.add_argument("--cpu-sample-chunks", type=int, default=4)  # = the reference arm's sample
     ap.add_argument("--no-swap-sweep", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1 / C4-block phase")
     ap.add_argument("--shard-blocks", type=int, default=2,
