@@ -61,10 +61,14 @@ def _inv(s):
     return {e["name"]: (e["pass"], e["detail"]) for e in s["invariants"]}
 
 
-def test_c1_overlapped_host_tier_matches_oracle(cuda_dev):
+@pytest.mark.parametrize("launch", ["graph", "stream"])
+def test_c1_overlapped_host_tier_matches_oracle(cuda_dev, launch):
+    """Both launch modes: the iteration captured once into a CUDA graph (the
+    default) and issued task by task on the lane streams."""
     chunks, ref = _chunks(cuda_dev)
-    st, s, err = graph_execute(scenario(), {"tier": "host", "compute_rate": RATE}, chunks)
+    st, s, err = graph_execute(scenario(), {"tier": "host", "compute_rate": RATE, "launch": launch}, chunks)
     assert st == 0, (err, _failing(s))
+    assert s["launch"] == launch
     assert s["all_invariants_pass"], s["invariants"]
     assert s["swap_mismatches"] == 0 and s["swap_checks"] == L  # one checkpoint per block
     pb = s["physical_bytes"]
@@ -84,13 +88,16 @@ def test_c1_b128_swapped_layers_round_trip(cuda_dev):
     assert s["physical_bytes"]["h2d/activations"] == s["reference_bytes"]["link_c2g/activations"]
 
 
-def test_c1_file_tier_checkpoints_on_ssd(cuda_dev, tmp_path):
-    # cpu_mem 1 GB forces the planner's checkpoint placement to SSD
+@pytest.mark.parametrize("launch", ["graph", "stream"])
+def test_c1_file_tier_checkpoints_on_ssd(cuda_dev, tmp_path, launch):
+    # cpu_mem 1 GB forces the planner's checkpoint placement to SSD; the file
+    # IO runs as host nodes of the captured graph / host functions on the lane
     sc = scenario(hardware='{"preset": "a100-12ssd", "cpu_mem": 1000000000}')
     chunks, ref = _chunks(cuda_dev, seed=100)
     st, s, err = graph_execute(sc, {"tier": "file", "file_dir": str(tmp_path),
-                                    "compute_rate": RATE}, chunks)
+                                    "compute_rate": RATE, "launch": launch}, chunks)
     assert st == 0, (err, _failing(s))
+    assert s["launch"] == launch
     assert s["checkpoint_location"] == "ssd"
     assert s["all_invariants_pass"], s["invariants"]
     assert s["swap_mismatches"] == 0 and s["swap_checks"] == L
