@@ -1033,7 +1033,8 @@ def iteration_phase(F):
     for tag, layers, heads, hidden, batch in (("c1_b8", 12, 12, 768, 8), ("c1_b8_resident", 12, 12, 768, 8),
                                               ("c1_b128", 12, 12, 768, 128),
                                               ("13b_shape_4_blocks_b8", 4, 40, 5120, 8),
-                                              ("13b_shape_4_blocks_b8_resident", 4, 40, 5120, 8)):
+                                              ("13b_shape_4_blocks_b8_resident", 4, 40, 5120, 8),
+                                              ("c1_b8_file_tier", 12, 12, 768, 8)):
         sc = json.dumps({"schema_version": 1, "model": {"name": tag, "num_layers": layers,
                          "num_heads": heads, "hidden_dim": hidden, "batch_size": batch, "seq_len": 1024},
                          "hardware": "a100-12ssd", "variant": "overlapped"})
@@ -1045,6 +1046,9 @@ def iteration_phase(F):
             # real bf16 GEMMs beside the optimizer; each wgrad writes its
             # block's gradients, which the fused optimizer then consumes
             opts = {"tier": "host", "compute_mode": "gemm_dataflow"}
+        if tag.endswith("_file_tier"):
+            # optimizer states and params in O_DIRECT files (the SSD tier)
+            opts = {**opts, "tier": "file", "file_dir": "/tmp/offsim_bench_file_tier"}
         if tag.endswith("_resident"):
             # all optimizer states stay in HBM (resident_groups): 1.0 GB for C1,
             # 15.1 GB for the 13B slice
