@@ -284,3 +284,46 @@ def test_shard_two_processes_ipc(cuda_dev, tier):
         for q, qr in zip(rsq, sqs):
             assert abs(q - qr) <= 1e-5 * qr
     assert got[0][2] == got[1][2]  # the same global norm on both ranks
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_shard_in_place_gradients_in_the_arena(cuda_dev, world):
+    """The reference's in-place convention on the product path (what the
+    bench's headline and INTEGRATION.md §4 do): each rank lands its slice's
+    gradients in its own slot of the chunk's arena region (own_params) and
+    the update overwrites them with the params — then the gather fills the
+    other slots. Two consecutive steps (the second step's grads written into
+    the slot again), bit-exact vs the oracle in every rank's arena."""
+    from paper_2403_06504_b200 import optim as F
+    inp = _inputs(SIZES, seed=40 + world)
+    shards = [F.Shard(SIZES, world=world, rank=r, gather="peer" if world > 1 else None, tier="device")
+              for r in range(world)]
+    if world > 1:
+        arenas = [s.arena() for s in shards]
+        for s in shards:
+            s.connect_ptrs(arenas)
+    bufs = [_shard_buffers(F, s, inp, cuda_dev, "device") for s in shards]
+    streams = _raw_streams(world)
+    steps = (10, 11)
+    ref, sqs = _oracle(inp, steps)
+    for i, step in enumerate(steps):
+        ios = []
+        for s, b in zip(shards, bufs):
+            io = []
+            for c, bb in enumerate(b):
+                slot = s.own_params(c)
+                if bb["cnt"]:
+                    slot.copy_(bb["grads"][i])  # the gradients land in the arena slot
+                io.append(dict(states=bb["states"].data_ptr() if bb["cnt"] else None,
+                               grad=slot.data_ptr() if bb["cnt"] else None))
+            ios.append(io)
+        torch.cuda.synchronize()
+        for s, io, st in zip(shards, ios, streams):
+            s.step(io, F.Hparams(step=step), want_grad_norm=True, stream=st)
+        for s in shards:
+            sq, bad = s.wait()
+            assert bad == 0 and abs(sq - sqs[i]) <= 1e-5 * sqs[i]
+    torch.cuda.synchronize()
+    _check(F, shards, bufs, ref, inp)
+    for s in shards:
+        s.close()
