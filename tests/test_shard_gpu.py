@@ -6,8 +6,8 @@ rank updates its slice and the updated bf16 params are all-gathered into
 every rank's arena. Results must equal the single-GPU oracle step of the
 WHOLE chunk bit for bit: every rank's states slice, every rank's full
 params, and the global grad norm (the per-rank sums are added in a
-different order than the oracle's element order: rel 1e-5, the fused
-kernel's bar).
+different order than the oracle's element order: rel 2e-7, the fused
+kernel's measured precision bar, test_adamw_gpu.test_grad_norm_precision).
 
 One GPU is available, so world > 1 runs as W shards on the same device —
 in one process (fy_shard_connect_ptrs, each shard's step on its own
@@ -121,7 +121,7 @@ def test_shard_world1_matches_oracle(cuda_dev, tier, nccl):
         sh.step(_io(bufs, i), F.Hparams(step=step), want_grad_norm=True)
         sq, bad = sh.wait()
         assert bad == 0
-        assert abs(sq - sqs[i]) <= 1e-5 * sqs[i]
+        assert abs(sq - sqs[i]) <= 2e-7 * sqs[i]
     torch.cuda.synchronize()
     _check(F, [sh], [bufs], ref, inp)
     st = sh.stats()
@@ -192,7 +192,7 @@ def single_process_peer(cuda_dev, world, tier):
         got = [s.wait() for s in shards]
         for sq, bad in got:
             assert bad == 0
-            assert abs(sq - sqs[i]) <= 1e-5 * sqs[i]
+            assert abs(sq - sqs[i]) <= 2e-7 * sqs[i]
         # every rank sums the per-rank partials in rank order: identical
         assert len({g[0] for g in got}) == 1
     torch.cuda.synchronize()
@@ -282,7 +282,7 @@ def test_shard_two_processes_ipc(cuda_dev, tier):
             for j, key in enumerate(("master", "m", "v")):
                 assert np.array_equal(st[j * cnt:(j + 1) * cnt].view(np.uint32), x[key][a:a + cnt].view(np.uint32))
         for q, qr in zip(rsq, sqs):
-            assert abs(q - qr) <= 1e-5 * qr
+            assert abs(q - qr) <= 2e-7 * qr
     assert got[0][2] == got[1][2]  # the same global norm on both ranks
 
 
@@ -322,7 +322,7 @@ def test_shard_in_place_gradients_in_the_arena(cuda_dev, world):
             s.step(io, F.Hparams(step=step), want_grad_norm=True, stream=st)
         for s in shards:
             sq, bad = s.wait()
-            assert bad == 0 and abs(sq - sqs[i]) <= 1e-5 * sqs[i]
+            assert bad == 0 and abs(sq - sqs[i]) <= 2e-7 * sqs[i]
     torch.cuda.synchronize()
     _check(F, shards, bufs, ref, inp)
     for s in shards:
