@@ -275,6 +275,10 @@ typedef struct fy_shard_config {
                                     unit (0 = a whole slice)                   */
     int params_to_host;          /* also D2H each updated slice to io.h_param  */
     int no_step_counter;
+    int grads_on_host;           /* io.grad is pinned HOST memory: each slice's
+                                    grads go H2D through the chunk pipeline
+                                    (with FY_TIER_DEVICE the states stay in
+                                    HBM; io.grad and io.h_param may alias)   */
 } fy_shard_config;
 
 typedef struct fy_shard_slice {
@@ -285,7 +289,8 @@ typedef struct fy_shard_slice {
 
 typedef struct fy_shard_io {     /* one per chunk: this rank's buffers         */
     void* states;                /* [master|m|v] of the slice, 12*count bytes  */
-    const void* grad;            /* device [count] gradients of the slice      */
+    const void* grad;            /* [count] gradients of the slice: device, or
+                                    pinned host with grads_on_host           */
     void* h_param;               /* pinned host [count] (params_to_host)       */
     void* grad_ready;            /* optional cudaEvent_t                       */
 } fy_shard_io;

@@ -87,7 +87,7 @@ class ShardConfig(C.Structure):
         ("nccl_id", C.c_void_p), ("tier", C.c_int), ("chunk_count", C.c_uint32),
         ("chunk_elems", C.POINTER(C.c_uint64)), ("grad_dtype", C.c_int), ("param_dtype", C.c_int),
         ("slots", C.c_uint32), ("piece_elems", C.c_uint64), ("params_to_host", C.c_int),
-        ("no_step_counter", C.c_int),
+        ("no_step_counter", C.c_int), ("grads_on_host", C.c_int),
     ]
 
 

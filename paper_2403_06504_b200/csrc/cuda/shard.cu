@@ -209,17 +209,19 @@ ShardGroup::ShardGroup(const fy_shard_config& cfg) : cfg_(cfg) {
                 connect_handles(h.data());
             }
         }
-        if (cfg_.tier == FY_TIER_HOST) {
+        if (cfg_.tier == FY_TIER_HOST || cfg_.grads_on_host) {
+            // streamed states and / or host gradients: the chunk pipeline
+            // moves them (device-tier states stay in place, states_on_device)
             fy_pipeline_config pc{};
             pc.device = cfg_.device;
             pc.max_chunk_elems = std::max<std::uint64_t>(max_piece, 8);
             pc.slots = cfg_.slots ? cfg_.slots : 3;
             pc.grad_dtype = cfg_.grad_dtype;
             pc.param_dtype = cfg_.param_dtype;
-            pc.grads_on_host = 0;
+            pc.grads_on_host = cfg_.grads_on_host ? 1 : 0;
             pc.params_to_host = cfg_.params_to_host;
             pc.keep_params_on_device = 1;  // the arena is the device copy
-            pc.states_on_device = 0;
+            pc.states_on_device = cfg_.tier == FY_TIER_DEVICE ? 1 : 0;
             pc.no_step_counter = 1;        // the shard passes each chunk's beta^t
             pipe_ = std::make_unique<ChunkPipeline>(pc);
         }
@@ -397,7 +399,7 @@ void ShardGroup::step(const fy_shard_io* io, const fy_adam_hparams& hp, bool wan
     gather_bytes_ = h2d_bytes_ = d2h_bytes_ = 0;
     check_cuda(cudaEventRecord(start_, stream), "record start");
     check_cuda(cudaStreamWaitEvent(comm_s_, start_, 0), "wait start");
-    if (cfg_.tier == FY_TIER_DEVICE) step_resident(io, hp, want_norm);
+    if (!pipe_) step_resident(io, hp, want_norm);
     else step_streamed(io, hp, want_norm);
     check_cuda(cudaMemcpyAsync(h_total_, d_total_, sizeof(double), cudaMemcpyDeviceToHost, comm_s_), "norm D2H");
     check_cuda(cudaMemcpyAsync(h_flags_, d_nonfinite_, 2 * sizeof(int), cudaMemcpyDeviceToHost, comm_s_),
@@ -501,8 +503,9 @@ void ShardGroup::step_streamed(const fy_shard_io* io, const fy_adam_hparams& hp,
             unit_chunk_.push_back(c);
         }
         has_unit[c] = true;
-        h2d_bytes_ += 12 * sl.count;
-        d2h_bytes_ += 12 * sl.count + (cfg_.params_to_host ? sl.count * pbytes_ : 0);
+        const std::uint64_t state_b = cfg_.tier == FY_TIER_HOST ? 12 * sl.count : 0;
+        h2d_bytes_ += state_b + (cfg_.grads_on_host ? sl.count * gbytes_ : 0);
+        d2h_bytes_ += state_b + (cfg_.params_to_host ? sl.count * pbytes_ : 0);
     }
     if (!units_.empty()) {
         pipe_->step(units_.data(), static_cast<std::uint32_t>(units_.size()), hp, want_norm, unit_hp_.data(),
@@ -553,7 +556,7 @@ void ShardGroup::update_ms(double* out, std::uint32_t count) const {
     if (count > cfg_.chunk_count) throw ArgError("shard: more chunks requested than the shard has");
     for (std::uint32_t c = 0; c < count; ++c) out[c] = 0.0;
     if (seq_ == 0) return;
-    if (cfg_.tier == FY_TIER_DEVICE) {
+    if (!pipe_) {
         for (std::uint32_t c = 0; c < count; ++c) {
             if (slices_[c].count == 0) continue;
             float ms = 0.0f;

@@ -336,7 +336,7 @@ class Shard:
                  gather: Optional[str] = None, nccl_id: Optional[bytes] = None, tier: str = "device",
                  grad_dtype: torch.dtype = torch.bfloat16, param_dtype: torch.dtype = torch.bfloat16,
                  slots: int = 0, piece_elems: int = 0, params_to_host: bool = False,
-                 no_step_counter: bool = False):
+                 no_step_counter: bool = False, grads_on_host: bool = False):
         self.chunk_elems = list(chunk_elems)
         self._elems = (C.c_uint64 * len(self.chunk_elems))(*self.chunk_elems)
         self._id = C.create_string_buffer(nccl_id, FY_NCCL_ID_BYTES) if nccl_id is not None else None
@@ -344,7 +344,7 @@ class Shard:
                           C.cast(self._id, C.c_void_p) if self._id is not None else None,
                           FY_TIER_HOST if tier == "host" else FY_TIER_DEVICE, len(self.chunk_elems),
                           self._elems, fy_dtype(grad_dtype), fy_dtype(param_dtype), slots, piece_elems,
-                          int(params_to_host), int(no_step_counter))
+                          int(params_to_host), int(no_step_counter), int(grads_on_host))
         h = C.c_void_p()
         check(LIB.fy_shard_create(C.byref(cfg), C.byref(h)))
         self._h = h

@@ -327,3 +327,54 @@ def test_shard_in_place_gradients_in_the_arena(cuda_dev, world):
     _check(F, shards, bufs, ref, inp)
     for s in shards:
         s.close()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_shard_host_gradients_device_states(cuda_dev, world):
+    """grads_on_host: HBM-resident states, the slice's gradients in pinned
+    HOST memory (H2D through the shard's chunk pipeline) and the updated
+    params D2H into the SAME host buffer (the e2e contract: host grads in,
+    host params out), plus the all-gather into every rank's arena. Two
+    steps, bit-exact vs the oracle: arena params, device states and the
+    host buffer (the rank's own slice of the params)."""
+    from paper_2403_06504_b200 import optim as F
+    inp = _inputs(SIZES, seed=60 + world)
+    shards = [F.Shard(SIZES, world=world, rank=r, gather="peer" if world > 1 else None, tier="device",
+                      grads_on_host=True, params_to_host=True) for r in range(world)]
+    if world > 1:
+        arenas = [s.arena() for s in shards]
+        for s in shards:
+            s.connect_ptrs(arenas)
+    bufs = [_shard_buffers(F, s, inp, cuda_dev, "device") for s in shards]
+    host = [[torch.empty(max(b["cnt"], 1), dtype=torch.bfloat16).pin_memory() for b in bb] for bb in bufs]
+    streams = _raw_streams(world)
+    steps = (10, 11)
+    ref, sqs = _oracle(inp, steps)
+    for i, step in enumerate(steps):
+        ios = []
+        for bb, hh in zip(bufs, host):
+            io = []
+            for b, h in zip(bb, hh):
+                if b["cnt"]:
+                    h[:b["cnt"]].copy_(b["grads"][i].cpu())   # this step's grads, host side
+                io.append(dict(states=b["states"].data_ptr() if b["cnt"] else None,
+                               grad=h.data_ptr() if b["cnt"] else None,
+                               h_param=h.data_ptr() if b["cnt"] else None))
+            ios.append(io)
+        for s, io, st in zip(shards, ios, streams):
+            s.step(io, F.Hparams(step=step), want_grad_norm=True, stream=st)
+        for s in shards:
+            sq, bad = s.wait()
+            assert bad == 0 and abs(sq - sqs[i]) <= 2e-7 * sqs[i]
+        st = shards[0].stats()
+        n_own = sum(b["cnt"] for b in bufs[0])
+        assert st["h2d_bytes"] == 2 * n_own and st["d2h_bytes"] == 2 * n_own
+    torch.cuda.synchronize()
+    _check(F, shards, bufs, ref, inp)
+    for r, (bb, hh) in enumerate(zip(bufs, host)):
+        for c, (b, h) in enumerate(zip(bb, hh)):
+            if b["cnt"]:
+                own = ref[c]["p"][b["off"]:b["off"] + b["cnt"]]
+                assert np.array_equal(h[:b["cnt"]].view(torch.int16).numpy().view(np.uint16), own), (r, c)
+    for s in shards:
+        s.close()
