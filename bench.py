@@ -677,20 +677,21 @@ def resident_phase(torch, F, args, world, rank, local):
 
 
 def e2e_phase(torch, F, args, states, cnt, world, rank, local):
-    """Same step through fy_pipeline_* with host grads in / host params out
-    (states of this rank's slice resident in HBM). N>1: each rank streams its
-    own slice; the kernel also writes the slice into the block's full-param
-    buffer on the device and the block's NCCL all-gather starts on a side
-    stream as soon as the block is updated (fy_chunk.update_done), overlapping
-    the next blocks' host-link traffic. Time: host wall clock, max over
-    ranks."""
-    import torch.distributed as dist
+    """The same step through the product's sharded entry point with HOST
+    buffers (fy_shard_*, grads_on_host + params_to_host): every rank's bf16
+    gradients go H2D from pinned host memory through the shard's chunk
+    pipeline, the update runs on its HBM-resident state slices, the updated
+    params come back D2H into the same host buffer (the reference
+    optimizer's inputs / outputs live in CPU memory,
+    task_graph.cpp:442-445,488-502) and, at N>1, each block's slice is
+    all-gathered into every rank's arena as soon as it is updated (PEER
+    copy-engine pushes or NCCL), overlapping the next blocks' host-link
+    traffic. Time: host wall clock around step + wait, max over ranks."""
     L = len(states)
     n = cnt
-    pad = (n + 7) // 8 * 8
+    N = 12 * args.hidden * args.hidden
+    torch.cuda.empty_cache()  # torch's cached blocks back to the driver: the shard's arena is cudaMalloc'd
     link_now = pcie_peaks(torch) if world == 1 else None
-    dev = torch.device("cuda", local)
-    full = [torch.empty(world * pad, dtype=torch.bfloat16, device=dev) for _ in range(L)] if world > 1 else None
     hbuf = []
     rng = np.random.default_rng(SEED + 77 + rank)
     for k in range(L):
@@ -704,29 +705,16 @@ def e2e_phase(torch, F, args, states, cnt, world, rank, local):
         arr = np.ctypeslib.as_array((C.c_uint16 * n).from_address(p.value))
         for a in range(0, n, pattern.size):
             arr[a:a + pattern.size] = pattern[:n - a]
-    done = [torch.cuda.Event() for _ in range(L)]
-    pipe = F.optim.ChunkPipeline(n, slots=4, grads_on_host=True, params_to_host=True,
-                                 keep_params_on_device=world > 1, states_on_device=True)
-    chunks = [dict(n=n, h_states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value,
-                   d_param=full[k][rank * pad:rank * pad + n].data_ptr() if world > 1 else None,
-                   update_done=done[k].cuda_event if world > 1 else None)
-              for k in range(L)]
-    for e in done:
-        e.record()  # create the events before the pipeline records into them
-    comm = torch.cuda.Stream(dev) if world > 1 else None
+    prefer = "nccl" if args.gather == "nccl" else "peer"
+    sh, gather, note = make_shard(torch, F, args, world, rank, local, [N] * L, "device", prefer, slots=4,
+                                  grads_on_host=True, params_to_host=True)
+    io = [dict(states=states[k].data_ptr(), grad=hbuf[k].value, h_param=hbuf[k].value) for k in range(L)]
     hp = F.optim.Hparams()
 
     def step(i):
         hp.step = i
-        pipe.step(chunks, hp, want_grad_norm=True)
-        if world > 1:  # per block, as soon as it is updated (overlaps the host link)
-            for k in range(L):
-                comm.wait_event(done[k])
-                with torch.cuda.stream(comm):
-                    dist.all_gather_into_tensor(full[k], full[k][rank * pad:(rank + 1) * pad])
-        pipe.wait()
-        if world > 1:
-            comm.synchronize()
+        sh.step(io, hp, want_grad_norm=True)
+        sh.wait()
 
     for w in range(args.warmup):
         step(1000 + w)
@@ -737,20 +725,22 @@ def e2e_phase(torch, F, args, states, cnt, world, rank, local):
         step(2000 + i)
     el = time.perf_counter() - t0
     el = max_over_ranks(el, world)
-    pipe.close()
+    st = sh.stats()
+    sh.close()
     for p in hbuf:
         F.check(F.LIB.fy_host_free(p))
-    del full
-    P = args.layers * 12 * args.hidden * args.hidden  # whole-job params per step
+    P = args.layers * N  # whole-job params per step
     return {
         "value": args.steps * P / el, "unit": UNIT,
         "h2d_bytes_per_step": 2 * L * n * world, "d2h_bytes_per_step": 2 * L * n * world,
         "ms_per_step": el / args.steps * 1e3,
         "link_gbs_each_way": 2 * L * n * args.steps / el / 1e9,
-        "path": "fy_pipeline_step (C ABI): host bf16 grads H2D -> fused AdamW on HBM-resident "
-                "states -> bf16 params D2H into the same host buffer; wall clock"
-                + ("; + per-block NCCL all-gather of the device-side bf16 slices, overlapped "
-                   "(fy_chunk.update_done)" if world > 1 else ""),
+        "path": "fy_shard_step (C ABI, grads_on_host + params_to_host): host bf16 grads H2D -> fused "
+                "AdamW on HBM-resident states -> bf16 params D2H into the same host buffer; wall clock"
+                + (f"; + per-block {gather} all-gather of the bf16 slices into every rank's arena, "
+                   "overlapped" if world > 1 else ""),
+        "gather": gather, "gather_note": note,
+        "shard_h2d_bytes_per_step": st["h2d_bytes"], "shard_d2h_bytes_per_step": st["d2h_bytes"],
         "launches": args.steps * L * 2,
         "grads": "bf16 of N(0, 1e-3^2) (SURVEY.md §8d)",
         "pcie_at_e2e": link_now,
