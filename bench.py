@@ -69,7 +69,6 @@ METRIC = "Adam params/sec & GB/s vs HBM/host-link roofline at 1/2/4/8 B200"
 UNIT = "params/s"
 BYTES_RESIDENT = 28  # 2 grad r + 12 state r + 12 state w + 2 param w
 SEED = 20240817
-E2E_PIECES = 1  # pipeline units per block in the e2e path (profiles/r01ae_e2e_shape_ab.txt)
 
 
 def shape(layers: int, hidden: int):
