@@ -378,3 +378,55 @@ def test_shard_host_gradients_device_states(cuda_dev, world):
                 assert np.array_equal(h[:b["cnt"]].view(torch.int16).numpy().view(np.uint16), own), (r, c)
     for s in shards:
         s.close()
+
+
+def test_shard_fp16_loss_scaled(cuda_dev):
+    """DeepSpeed's fp16 mode through the sharded step: fp16 gradients at a
+    loss scale of 2^16 (grad_scale 2^-16), fp16 params gathered into every
+    rank's arena; W = 2 in one process, two steps, bit-exact vs the oracle
+    (same unscale arithmetic) in states and params."""
+    from paper_2403_06504_b200 import optim as F
+    sizes = [4099, 3 * 2048 * 17 + 40, 8]
+    world, scale = 2, 2.0 ** -16
+    rng = np.random.default_rng(20240901)
+    inp = []
+    for n in sizes:
+        g = [torch.from_numpy((rng.normal(0, 1e-3, n) / scale).astype(np.float32)).to(torch.float16)
+             .view(torch.int16).numpy().view(np.uint16).copy() for _ in range(2)]
+        inp.append(dict(master=rng.normal(0, 0.02, n).astype(np.float32),
+                        m=rng.normal(0, 1e-3, n).astype(np.float32),
+                        v=(rng.normal(0, 1e-3, n) ** 2).astype(np.float32), g=g))
+    # oracle: whole chunks, DeepSpeed counter, fp16 grads / params
+    ref = [dict(master=c["master"].copy(), m=c["m"].copy(), v=c["v"].copy(), p=np.zeros(c["master"].size, np.uint16))
+           for c in inp]
+    k = O.StepCounter()
+    steps = (10, 11)
+    for i, step in enumerate(steps):
+        for c, r in zip(inp, ref):
+            O.adamw_step(r["master"], r["m"], r["v"], c["g"][i], O.FP16, O.scalars_bt(*k.next(step)),
+                         grad_scale=scale, param_out=r["p"], param_dtype=O.FP16)
+    shards = [F.Shard(sizes, world=world, rank=r, gather="peer", tier="device", grad_dtype=torch.float16,
+                      param_dtype=torch.float16) for r in range(world)]
+    arenas = [s.arena() for s in shards]
+    for s in shards:
+        s.connect_ptrs(arenas)
+    bufs = []
+    for s in shards:
+        b = []
+        for c, x in enumerate(inp):
+            sl = s.slice(c)
+            a, e = sl["offset"], sl["offset"] + sl["count"]
+            st = torch.from_numpy(np.concatenate([x["master"][a:e], x["m"][a:e], x["v"][a:e]])).to(cuda_dev)
+            gr = [torch.from_numpy(g[a:e].view(np.int16).copy()).view(torch.float16).to(cuda_dev) for g in x["g"]]
+            b.append(dict(states=st, grads=gr, off=a, cnt=e - a))
+        bufs.append(b)
+    streams = _raw_streams(world)
+    for i, step in enumerate(steps):
+        for s, b, st in zip(shards, bufs, streams):
+            s.step(_io(b, i), F.Hparams(step=step, grad_scale=scale), stream=st)
+        for s in shards:
+            s.wait()
+    torch.cuda.synchronize()
+    _check(F, shards, bufs, ref, inp)
+    for s in shards:
+        s.close()
