@@ -321,8 +321,10 @@ fy_status fy_shard_step(fy_shard* s, const fy_shard_io* io, const fy_adam_hparam
 fy_status fy_shard_wait(fy_shard* s, double* grad_sq_sum, int* nonfinite);
 fy_status fy_shard_get_stats(const fy_shard* s, fy_shard_stats* out);
 /* Device time of each chunk's update kernel(s) in the last waited step, ms
- * (events around the launches on the shard's update stream; streamed tier:
- * the sum over the chunk's pipeline pieces). */
+ * (resident: one event per chunk on the shard's update stream, the chunk's
+ * fused update + norm reduction from the previous chunk's end, the step's
+ * start or its grad_ready; streamed tier: the sum over the chunk's pipeline
+ * pieces' update kernels). */
 fy_status fy_shard_update_ms(const fy_shard* s, double* chunk_ms, uint32_t count);
 
 /* ------------------------------------------------------------------ */

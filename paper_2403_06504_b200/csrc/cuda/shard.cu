@@ -163,11 +163,15 @@ ShardGroup::ShardGroup(const fy_shard_config& cfg) : cfg_(cfg) {
         check_cuda(cudaEventCreate(&done_), "event");
         check_cuda(cudaEventCreateWithFlags(&upd_all_, cudaEventDisableTiming), "event");
         chunk_ev_.resize(cfg_.chunk_count);
-        for (cudaEvent_t& e : chunk_ev_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-        upd_t0_.resize(cfg_.chunk_count);
-        upd_t1_.resize(cfg_.chunk_count);
+        // chunk_ev_ marks each chunk's end (gather / D2H waits) and, timed,
+        // doubles as the next chunk's start for update_ms: one event per
+        // chunk on the update stream (each record is a few us of device time
+        // between the kernels; r02am: 3 per chunk cost 0.25 ms per 13B step)
+        for (cudaEvent_t& e : chunk_ev_) check_cuda(cudaEventCreate(&e), "event");
+        upd_t0_.resize(cfg_.chunk_count);  // only after a grad_ready wait
         for (cudaEvent_t& e : upd_t0_) check_cuda(cudaEventCreate(&e), "event");
-        for (cudaEvent_t& e : upd_t1_) check_cuda(cudaEventCreate(&e), "event");
+        check_cuda(cudaEventCreate(&upd_start_), "event");
+        t0_recorded_.assign(cfg_.chunk_count, 0);
         // every kernel a step may launch is loaded now, before any device
         // barrier can spin (lazy loading would deadlock behind it)
         const void* anchors[] = {reinterpret_cast<const void*>(shard_barrier_kernel)};
@@ -241,11 +245,11 @@ void ShardGroup::release() noexcept {
     comm_ = nullptr;
     for (void* p : opened_) cudaIpcCloseMemHandle(p);
     opened_.clear();
-    for (auto* v : {&chunk_ev_, &upd_t0_, &upd_t1_}) {
+    for (auto* v : {&chunk_ev_, &upd_t0_}) {
         for (cudaEvent_t e : *v) cudaEventDestroy(e);
         v->clear();
     }
-    for (cudaEvent_t* e : {&start_, &done_, &upd_all_})
+    for (cudaEvent_t* e : {&start_, &done_, &upd_all_, &upd_start_})
         if (*e) cudaEventDestroy(*e), *e = nullptr;
     if (opt_) cudaStreamDestroy(opt_);
     if (comm_s_) cudaStreamDestroy(comm_s_);
@@ -415,11 +419,18 @@ void ShardGroup::step_resident(const fy_shard_io* io, const fy_adam_hparams& hp,
     check_cuda(cudaMemsetAsync(d_nonfinite_, 0, sizeof(int), opt_), "memset");
     const bool peer = cfg_.gather == FY_GATHER_PEER;
     if (peer) barrier(kEntry, opt_, nullptr, nullptr);  // every peer may now receive this step's params
+    check_cuda(cudaEventRecord(upd_start_, opt_), "record");
     for (std::uint32_t c = 0; c < cfg_.chunk_count; ++c) {
         const Slice& sl = slices_[c];
         const fy_adam_hparams h = chunk_hp(hp);
-        if (io[c].grad_ready)
+        t0_recorded_[c] = 0;
+        if (io[c].grad_ready) {
             check_cuda(cudaStreamWaitEvent(opt_, static_cast<cudaEvent_t>(io[c].grad_ready), 0), "wait grad");
+            // the chunk's time starts when its gradients are ready, not at
+            // the previous chunk's end
+            check_cuda(cudaEventRecord(upd_t0_[c], opt_), "record");
+            t0_recorded_[c] = 1;
+        }
         if (sl.count > 0) {
             AdamLaunch a{};
             float* st = static_cast<float*>(io[c].states);
@@ -443,9 +454,7 @@ void ShardGroup::step_resident(const fy_shard_io* io, const fy_adam_hparams& hp,
                 }
                 gather_bytes_ += (cfg_.world - 1) * sl.count * pbytes_;
             }
-            check_cuda(cudaEventRecord(upd_t0_[c], opt_), "record");
             check_cuda(launch_adamw(a, opt_), "adamw launch (shard)");
-            check_cuda(cudaEventRecord(upd_t1_[c], opt_), "record");
         }
         check_cuda(cudaEventRecord(chunk_ev_[c], opt_), "record chunk");
         if (cfg_.gather == FY_GATHER_NCCL) {
@@ -557,11 +566,15 @@ void ShardGroup::update_ms(double* out, std::uint32_t count) const {
     for (std::uint32_t c = 0; c < count; ++c) out[c] = 0.0;
     if (seq_ == 0) return;
     if (!pipe_) {
+        // chunk c ran from the previous chunk's end (or the step's start,
+        // or its grad_ready) to its own end: its update + norm reduction
+        cudaEvent_t prev = upd_start_;
         for (std::uint32_t c = 0; c < count; ++c) {
-            if (slices_[c].count == 0) continue;
+            if (t0_recorded_[c]) prev = upd_t0_[c];
             float ms = 0.0f;
-            check_cuda(cudaEventElapsedTime(&ms, upd_t0_[c], upd_t1_[c]), "elapsed");
-            out[c] = ms;
+            check_cuda(cudaEventElapsedTime(&ms, prev, chunk_ev_[c]), "elapsed");
+            if (slices_[c].count > 0) out[c] = ms;
+            prev = chunk_ev_[c];
         }
     } else if (!units_.empty()) {
         std::vector<fy_chunk_timing> t(units_.size());

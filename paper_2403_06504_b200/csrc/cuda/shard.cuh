@@ -96,7 +96,9 @@ private:
     cudaStream_t opt_ = nullptr, comm_s_ = nullptr;
     cudaEvent_t start_ = nullptr, done_ = nullptr, upd_all_ = nullptr;
     std::vector<cudaEvent_t> chunk_ev_;
-    std::vector<cudaEvent_t> upd_t0_, upd_t1_;  // timed, around each chunk's update (resident)
+    std::vector<cudaEvent_t> upd_t0_;      // timed: after a chunk's grad_ready wait (resident)
+    std::vector<char> t0_recorded_;        // upd_t0_[c] recorded this step
+    cudaEvent_t upd_start_ = nullptr;      // timed: the resident step's first chunk may start
     std::vector<std::uint32_t> unit_chunk_;      // streamed: the chunk of every pipeline unit
     std::unique_ptr<ChunkPipeline> pipe_;
     std::vector<fy_chunk> units_;
