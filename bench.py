@@ -666,6 +666,35 @@ def resident_phase(torch, F, args, world, rank, local):
                               "launches_per_step": (2 * L if N // 2048 >= 16384 else 2 * (-(-L // 96))),
                               "note": "fy_adamw_chunks over the 40 chunks; chunks this large keep one "
                                       "launch each inside the call (profiles/r01z_multi_chunk_ab.txt)"}
+        # the same step with global grad-norm clipping (GPT-3 clips at 1.0):
+        # fy_grad_stats over every chunk (2 B/param read) -> fy_clip_coef on
+        # the device -> the fused step with the device-side scale / skip flag;
+        # no host round trip. 30 B/param moved.
+        scale = torch.ones(1, dtype=torch.float32, device=dev)
+        skip = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        def clipped():
+            for k in range(L):
+                F.optim.grad_stats(grads[k], 1.0, sq, ws, bad, accumulate=k > 0)
+            F.optim.clip_coef(sq, bad, 1.0, scale, skip)
+            F.optim.adamw_chunks(multi, hp, grad_scale_dev=scale, skip_if_set=skip)
+
+        clipped()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for s_ in range(args.steps):
+            hp.step = 200 + s_
+            clipped()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms_clip = a.elapsed_time(b) / args.steps
+        peak_c, _ = peaks()
+        res["clipped_step"] = {"ms_per_step": ms_clip, "params_per_s": P / (ms_clip * 1e-3),
+                               "gbs_at_30B": 30 * P / (ms_clip * 1e-3) / 1e9,
+                               "frac_of_hbm_peak": 30 * P / (ms_clip * 1e-3) / 1e9 / peak_c,
+                               "clip_coef": float(scale.item()), "skipped": int(skip.item()),
+                               "path": "fy_grad_stats x 40 -> fy_clip_coef -> fy_adamw_chunks (device-side "
+                                       "scale / skip), max_norm 1.0"}
     sh.close()
     del io
     if not args.no_e2e:
@@ -1440,6 +1469,7 @@ def main():
                      "kernel_share_of_step": res["kernel_share"]},
         "clocks": res["clocks"],
         "multi_chunk_step": res.get("multi_chunk"),
+        "clipped_step": res.get("clipped_step"),
         "gpu_launches": res["launches"] + (res.get("e2e", {}).get("launches", 0)),
     }
     if "e2e" in res:
