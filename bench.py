@@ -1214,7 +1214,7 @@ def swap_sweep_phase(F, budget_cpu=32e9, budget_ssd=16e9):
                          "executed_blocks": blocks, "makespan_s": d.get("executed", {}).get("makespan_s"),
                          "legs": legs, "all_invariants_pass": d.get("all_invariants_pass"),
                          "swap_checks": d.get("swap_checks"), "swap_mismatches": d.get("swap_mismatches"),
-                         "io_engine": d.get("io_engine")})
+                         "io_engine": d.get("io_engine"), "file_warmup_s": d.get("file_warmup_s")})
         L.offsim_scenario_free(hnd)
     return rows
 

@@ -66,6 +66,14 @@ struct ExecOptions {
     bool direct_io = true;          // O_DIRECT for the file tier
     bool fixed_buffers = true;      // register the staging rings with io_uring (READ/WRITE_FIXED)
     std::uint32_t io_depth = 32;    // io_uring requests in flight PER tier device (file_dirs entry)
+    // Before calibration and the timed iteration, bring the file lane to the
+    // state every iteration after the first finds it: each activation /
+    // checkpoint / gradient file extent written once and each host buffer a
+    // file read lands in DMA-written once. Cold, the first write to a new
+    // extent and the first device DMA into a host region run ~1.6x slower on
+    // the leases' virtio disk (profiles/r02aq_file_rw_*.txt), so a single
+    // cold iteration would measure first-touch costs, not the file lane.
+    bool warm_files = true;
     double compute_rate = 0.0;      // FLOP/s of synthetic compute (0: hw.gpu_tput)
     // fwd/bwd compute tasks: "spin" = timed kernel of work / compute_rate
     // (no SM/HBM contention); "gemm" = the layer's real bf16 GEMMs through
@@ -251,6 +259,7 @@ struct ExecReport {
     std::uint64_t io_registered_bytes = 0; // staging rings registered with io_uring
     std::uint64_t io_fixed_requests = 0;   // file requests issued as READ/WRITE_FIXED
     std::uint64_t io_plain_requests = 0;   // ... and as plain READ/WRITE
+    double file_warmup_s = 0.0;            // warm_files: untimed setup IO before calibration
     std::uint64_t pinned_host_bytes = 0;  // host staging the run allocated
     RingDepths host_ring;                 // staging ring depths (file tier)
     std::uint64_t state_checksum = 0;     // checksum_states

@@ -44,7 +44,7 @@ ParsedOptions parse_options(const char* text) {
                                                "swap_only", "max_blocks", "placement",
                                                "compute_mode", "host_ring", "checksum_states",
                                                "resident_groups", "fixed_buffers", "io_depth",
-                                               "launch"};
+                                               "launch", "warm_files"};
     for (const auto& it : doc.items())
         if (!keys.count(it.key())) throw ConfigError("unknown key '" + it.key() + "' in exec options");
     try {
@@ -68,6 +68,7 @@ ParsedOptions parse_options(const char* text) {
         o.direct_io = doc.value("direct_io", o.direct_io);
         o.fixed_buffers = doc.value("fixed_buffers", o.fixed_buffers);
         o.io_depth = doc.value("io_depth", o.io_depth);
+        o.warm_files = doc.value("warm_files", o.warm_files);
         o.launch = doc.value("launch", o.launch);
         if (o.launch != "graph" && o.launch != "stream")
             throw ConfigError("exec options: launch must be \"graph\" or \"stream\"");
@@ -278,6 +279,7 @@ std::string exec_summary_json(const ExecReport& r) {
         {"io_requests", {{"registered_bytes", r.io_registered_bytes},
                          {"fixed", r.io_fixed_requests},
                          {"plain", r.io_plain_requests}}},
+        {"file_warmup_s", r.file_warmup_s},
         {"pinned_host_bytes", r.pinned_host_bytes},
         {"host_ring", rings_json(r.host_ring)},
         {"state_checksum", r.state_checksum},

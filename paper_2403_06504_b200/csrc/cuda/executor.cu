@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <set>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -301,10 +302,19 @@ public:
     std::uint64_t io_fixed() const { return io_.fixed_requests(); }
     std::uint64_t io_plain() const { return io_.plain_requests(); }
     void run(const SimTrace& planned, ExecReport& rep);
+    double warm_file_lane();
 
 private:
     cudaStream_t lane_stream(ResourceId r) const { return streams_[static_cast<int>(r)]; }
     void issue(const Task& t, ExecReport& rep);
+    // the file-lane request of a task: tier file, host buffer, bytes, offset
+    struct FileOp {
+        const TierFile* file = nullptr;
+        void* buf = nullptr;
+        std::uint64_t bytes = 0, offset = 0;
+        bool write = false, poison = false;
+    };
+    bool file_op(const Task& t, FileOp& op);  // false: not a file request
     void issue_compute(const Task& t, const Parsed& p, cudaStream_t s, bool replay);
     std::uint64_t layer_offset(int j) const; // byte offset of layer j inside the block params
 
@@ -897,39 +907,47 @@ MeasuredRates Engine::calibrate() {
         // has been written, so a device / host cache cannot serve the
         // replay from one hot 512 MiB region (r01an: a 2 GiB single-region
         // replay predicted 5.6 GB/s where 75 GB of iteration IO got 4.0)
+        // Two passes, the second one timed: like the iteration after
+        // warm_file_lane, the replay then overwrites extents it has written
+        // before and reads into a buffer the device has written before
+        // (a cold first pass runs ~1.3-1.6x slower on the virtio disk).
         constexpr std::uint64_t kReplay = 8ull << 30;
         double rd_b = 0, rd_s = 0, wr_b = 0, wr_s = 0;
-        std::uint64_t wcur = round_up(bytes), written = round_up(bytes), rcur = 0, scur = 0;
-        for (const Task& t : g_.tasks) {
-            if (t.resource != ResourceId::link_ssd || t.work <= 0.0) continue;
-            if (rd_b + wr_b >= double(kReplay)) break;
-            const std::uint64_t b = round_up(std::min<std::uint64_t>(static_cast<std::uint64_t>(t.work), bytes));
-            IoRequest op = w;
-            op.bytes = b;
-            op.write = t.dir == TransferDir::c2s;
-            if (op.write) {
-                if (wcur + b > kReplay) wcur = 0;
-                op.offset = wcur;
-                wcur += b;
-                written = std::max(written, wcur);
-            } else if (f_states_ && tier_states_bytes_ >= b) {
-                // reads come from the real states file (written at setup,
-                // not since), like the iteration's own state reads, rather
-                // than from probe data written a moment before
-                if (scur + b > tier_states_bytes_) scur = 0;
-                op.file = f_states_->stripe();
-                op.offset = scur;
-                scur += b;
-            } else {
-                if (rcur + b > written) rcur = 0;
-                op.offset = rcur;
-                rcur += b;
+        std::uint64_t written = round_up(bytes);
+        for (int pass = 0; pass < (opt_.warm_files ? 2 : 1); ++pass) {
+            rd_b = rd_s = wr_b = wr_s = 0;
+            std::uint64_t wcur = round_up(bytes), rcur = 0, scur = 0;
+            for (const Task& t : g_.tasks) {
+                if (t.resource != ResourceId::link_ssd || t.work <= 0.0) continue;
+                if (rd_b + wr_b >= double(kReplay)) break;
+                const std::uint64_t b = round_up(std::min<std::uint64_t>(static_cast<std::uint64_t>(t.work), bytes));
+                IoRequest op = w;
+                op.bytes = b;
+                op.write = t.dir == TransferDir::c2s;
+                if (op.write) {
+                    if (wcur + b > kReplay) wcur = 0;
+                    op.offset = wcur;
+                    wcur += b;
+                    written = std::max(written, wcur);
+                } else if (f_states_ && tier_states_bytes_ >= b) {
+                    // reads come from the real states file (written at setup,
+                    // not since), like the iteration's own state reads, rather
+                    // than from probe data written a moment before
+                    if (scur + b > tier_states_bytes_) scur = 0;
+                    op.file = f_states_->stripe();
+                    op.offset = scur;
+                    scur += b;
+                } else {
+                    if (rcur + b > written) rcur = 0;
+                    op.offset = rcur;
+                    rcur += b;
+                }
+                const auto t0 = std::chrono::steady_clock::now();
+                run_io(&op);
+                const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                (op.write ? wr_b : rd_b) += static_cast<double>(b);
+                (op.write ? wr_s : rd_s) += sec;
             }
-            const auto t0 = std::chrono::steady_clock::now();
-            run_io(&op);
-            const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            (op.write ? wr_b : rd_b) += static_cast<double>(b);
-            (op.write ? wr_s : rd_s) += sec;
         }
         if (rd_s > 0) r.file_read_effective_bps = rd_b / rd_s;
         if (wr_s > 0) r.file_write_effective_bps = wr_b / wr_s;
@@ -1139,6 +1157,75 @@ void Engine::issue_compute(const Task& t, const Parsed& p, cudaStream_t s, bool 
     check_cuda(cudaGetLastError(), "compute launch");
 }
 
+bool Engine::file_op(const Task& t, FileOp& op) {
+    if (t.resource != ResourceId::link_ssd || t.work <= 0.0) return false;
+    const Parsed p = parse_name(t.name);
+    const std::uint32_t k = p.block;
+    const int j = p.layer;
+    const std::uint64_t li = j >= 0 ? 4ull * k + j : 0;
+    const std::uint64_t state_b = 12 * n_, param_b = 2 * n_;
+    const std::string& w = p.what;
+    if (w == "state_s2c" || w == "state_c2s") {
+        op = {f_states_.get(), host_states(t.id, k), state_b, k * round_up(state_b), w == "state_c2s", false};
+    } else if (w == "param_c2s") {
+        op = {f_params_.get(), host_params(t.id, k), param_b, k * round_up(param_b), true, false};
+    } else if (w == "p_s2c") {
+        const std::uint64_t off = layer_offset(j);
+        op = {f_params_.get(), host_weights(t.id, k, off), layers_[li].param_bytes, k * round_up(param_b) + off,
+              false, false};
+    } else if (w == "act_c2s" || w == "act_s2c") {
+        const bool wr = w == "act_c2s";
+        op = {f_acts_.get(), host_act(t.id, act_host_[li]), layers_[li].act_bytes, act_file_off_[li], wr,
+              wr && opt_.verify_swaps};
+    } else if (w == "ckpt_c2s" || w == "ckpt_s2c") {
+        const bool wr = w == "ckpt_c2s";
+        op = {f_acts_.get(), host_act(t.id, ckpt_host_[k]), ckpt_bytes_, ckpt_file_off_[k], wr,
+              wr && opt_.verify_swaps};
+    } else if (w == "grad_c2s" || w == "grad_s2c") {
+        op = {f_grads_.get(), grad_host_[k].p, param_b, k * round_up(param_b), w == "grad_c2s", false};
+    } else {
+        return false;
+    }
+    if (!op.file) throw InvariantError("executor: no tier file for task '" + t.name + "'");
+    return true;
+}
+
+// Untimed, before calibration: the file lane as every iteration after the
+// first finds it (ExecOptions::warm_files). (1) Every extent the iteration
+// WRITES in the activation / checkpoint / gradient files is written once
+// (setup already wrote the state and param files); (2) every host buffer a
+// file READ lands in receives one read (of its own extent). On the leases'
+// virtio disk the first write to a new extent runs at ~3.6-3.9 GB/s against
+// ~5 GB/s for an overwrite, and the first device DMA into a host region at
+// ~2.8 GB/s against ~4.6 (profiles/r02aq_file_rw_*.txt) — one cold
+// iteration measured first-touch costs, not the lane. Contents: the writes
+// only allocate extents that the iteration overwrites before reading them;
+// state / param reads return the bytes those buffers already hold (the
+// tier files were written from them at setup), and activation / gradient
+// buffers are overwritten by their D2H before any use.
+double Engine::warm_file_lane() {
+    if (!file_tier_ || !opt_.warm_files) return 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::set<std::pair<const void*, std::uint64_t>> written, read;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (const Task& t : g_.tasks) {
+            FileOp op;
+            if (!file_op(t, op) || op.write != (pass == 0)) continue;
+            if (op.write && op.file != f_acts_.get() && op.file != f_grads_.get()) continue;
+            auto& seen = op.write ? written : read;
+            // writes: every extent once; reads: every host buffer once
+            if (!seen.emplace(op.write ? static_cast<const void*>(op.file) : op.buf, op.write ? op.offset : 0)
+                     .second)
+                continue;
+            IoRequest r{&io_, op.file->stripe(), op.buf, round_up(op.bytes), op.offset, op.write, false,
+                        &io_error_, &io_error_text_, &io_mu_};
+            run_io(&r);
+        }
+    }
+    if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 void Engine::issue(const Task& t, ExecReport& rep) {
     cudaStream_t s = lane_stream(t.resource);
     for (const std::uint32_t d : t.deps)
@@ -1210,42 +1297,21 @@ void Engine::issue(const Task& t, ExecReport& rep) {
         d2h(host_states(t.id, k), slots_[slot_of(k)].p, state_b);
     } else if (w == "param_d2h") {
         d2h(host_params(t.id, k), d_grads_[k], param_b);
-    } else if (w == "state_s2c") {
-        file(*f_states_, host_states(t.id, k), state_b, k * round_up(state_b), false, false);
-    } else if (w == "state_c2s") {
-        file(*f_states_, host_states(t.id, k), state_b, k * round_up(state_b), true, false);
-    } else if (w == "param_c2s") {
-        file(*f_params_, host_params(t.id, k), param_b, k * round_up(param_b), true, false);
-    } else if (w == "p_s2c") {
-        const std::uint64_t off = layer_offset(j);
-        file(*f_params_, host_weights(t.id, k, off), layers_[li].param_bytes,
-             k * round_up(param_b) + off, false, false);
+    } else if (FileOp op; file_op(t, op)) {
+        file(*op.file, op.buf, op.bytes, op.offset, op.write, op.poison);
     } else if (w == "p_c2g") {
         void* dst = wscratch_[wscratch_turn_ ^= 1].p;
         h2d(dst, host_weights(t.id, k, layer_offset(j)), layers_[li].param_bytes);
     } else if (w == "act_g2c") {
         d2h(host_act(t.id, act_host_[li]), act_dev_[li].p, layers_[li].act_bytes);
-    } else if (w == "act_c2s") {
-        file(*f_acts_, host_act(t.id, act_host_[li]), layers_[li].act_bytes, act_file_off_[li], true,
-             opt_.verify_swaps);
-    } else if (w == "act_s2c") {
-        file(*f_acts_, host_act(t.id, act_host_[li]), layers_[li].act_bytes, act_file_off_[li], false, false);
     } else if (w == "act_c2g") {
         h2d(act_restore_[li].p, host_act(t.id, act_host_[li]), layers_[li].act_bytes);
     } else if (w == "ckpt_g2c") {
         d2h(host_act(t.id, ckpt_host_[k]), ckpt_dev_[k].p, ckpt_bytes_);
-    } else if (w == "ckpt_c2s") {
-        file(*f_acts_, host_act(t.id, ckpt_host_[k]), ckpt_bytes_, ckpt_file_off_[k], true, opt_.verify_swaps);
-    } else if (w == "ckpt_s2c") {
-        file(*f_acts_, host_act(t.id, ckpt_host_[k]), ckpt_bytes_, ckpt_file_off_[k], false, false);
     } else if (w == "ckpt_c2g") {
         h2d(ckpt_restore_[k].p, host_act(t.id, ckpt_host_[k]), ckpt_bytes_);
     } else if (w == "grad_g2c") {
         d2h(grad_host_[k].p, d_grads_[k], param_b);
-    } else if (w == "grad_c2s") {
-        file(*f_grads_, grad_host_[k].p, param_b, k * round_up(param_b), true, false);
-    } else if (w == "grad_s2c") {
-        file(*f_grads_, grad_host_[k].p, param_b, k * round_up(param_b), false, false);
     } else if (w == "grad_h2d") {
         h2d(const_cast<void*>(d_grads_[k]), grad_host_[k].p, param_b);
     } else {
@@ -1453,6 +1519,7 @@ ExecReport execute(const ModelConfig& model, const HardwareConfig& hw, const Swa
         rep.io_engine = eng.io_engine();
         rep.file_devices = static_cast<std::uint32_t>(eng.file_dirs().size());
     }
+    rep.file_warmup_s = eng.warm_file_lane();
     MeasuredRates rates = eng.calibrate();
     rep.io_registered_bytes = eng.io_registered();
     const std::uint64_t cal_fixed = eng.io_fixed(), cal_plain = eng.io_plain();
