@@ -510,6 +510,12 @@ def streamed_backward_overlap(torch, pipe, chunks, hp, K, P, t_stream):
             # 1.0 = the shorter of the two is fully hidden; values a little
             # above 1 are link run-to-run variance (t_both < t_stream alone)
             "overlap_efficiency": (t_stream + t_bwd - t_both) / min(t_stream, t_bwd),
+            # no update (hence no D2H) can start before block 0's backward
+            # ends: that first block's backward is exposed by construction,
+            # as in the reference's schedule (bwd of block k gates opt update
+            # gK). Of the rest of the backward, this fraction was hidden.
+            "first_block_backward_s": t_bwd / K,
+            "overlap_efficiency_after_first_block": (t_stream + t_bwd - t_both) / (t_bwd * (K - 1) / K),
             "value": K * C3["chunk"] / t_both, "unit": UNIT,
             "backward": "bf16 cuBLAS GEMMs (torch.matmul) of the 65B block, b=16 s=1024, "
                         "72*t*h^2 FLOPs/block, separate stream"}
