@@ -245,3 +245,31 @@ def test_resident_groups_same_states_fewer_bytes(cuda_dev, tmp_path, tier, R):
     pb0, pb1 = s0["physical_bytes"], s1["physical_bytes"]
     assert pb1.get("h2d/opt_states", 0) == pb0["h2d/opt_states"] - r * 12 * n
     assert pb1.get("d2h/opt_states", 0) == pb0["d2h/opt_states"] - r * 12 * n
+
+
+def test_warm_file_lane_changes_no_result(cuda_dev, tmp_path):
+    # warm_files (default on) writes the activation / checkpoint extents once
+    # and DMA-reads once into every file-read target before calibration: the
+    # final states must equal the cold run's and the host tier's bit for bit
+    # (ring and per-chunk host copies), every checkpoint must still round-trip
+    # through the file, and the setup IO is reported, untimed
+    sc = scenario(hardware='{"preset": "a100-12ssd", "cpu_mem": 1000000000}')
+    base = {"compute_rate": RATE, "checksum_states": True, "seed": 9}
+    st, host, _, err = execute(sc, dict(base, tier="host"))
+    assert st == 0, (err, _failing(host))
+    assert host["file_warmup_s"] == 0.0
+    for ring in (0, 2):
+        runs = {}
+        for warm in (True, False):
+            st, s, _, err = execute(sc, dict(base, tier="file", file_dir=str(tmp_path), host_ring=ring,
+                                             warm_files=warm))
+            assert st == 0, (err, _failing(s))
+            assert s["all_invariants_pass"] and s["swap_mismatches"] == 0 and s["swap_checks"] == L
+            assert s["checkpoint_location"] == "ssd"
+            runs[warm] = s
+        assert runs[True]["state_checksum"] == runs[False]["state_checksum"] == host["state_checksum"] != 0
+        assert runs[True]["file_warmup_s"] > 0.0 and runs[False]["file_warmup_s"] == 0.0
+        # the warm-up's requests are not the iteration's
+        assert runs[True]["io_requests"]["fixed"] + runs[True]["io_requests"]["plain"] == \
+            runs[False]["io_requests"]["fixed"] + runs[False]["io_requests"]["plain"]
+        assert runs[True]["physical_bytes"] == runs[False]["physical_bytes"]
