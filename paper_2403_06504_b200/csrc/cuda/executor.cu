@@ -900,52 +900,44 @@ MeasuredRates Engine::calibrate() {
         }
         r.file_write_bps = bytes / best_w;
         r.file_read_bps = bytes / best_r;
-        // effective: replay the graph's own file-lane operations in task
-        // order (each <= the probe size, <= 8 GiB in total) — reads and
-        // writes interleaved as the iteration issues them, writes at a
-        // moving cursor over an 8 GiB region and reads cycling over what
-        // has been written, so a device / host cache cannot serve the
-        // replay from one hot 512 MiB region (r01an: a 2 GiB single-region
-        // replay predicted 5.6 GB/s where 75 GB of iteration IO got 4.0)
-        // Two passes, the second one timed: like the iteration after
-        // warm_file_lane, the replay then overwrites extents it has written
-        // before and reads into a buffer the device has written before
-        // (a cold first pass runs ~1.3-1.6x slower on the virtio disk).
-        constexpr std::uint64_t kReplay = 8ull << 30;
+        // effective: replay the graph's own file-lane requests in task
+        // order (<= 4 GiB of reads and <= 4 GiB of writes per pass, so a
+        // write-heavy prefix cannot leave the reads unsampled) through the
+        // iteration's own host buffers
+        // and file extents (FileOp), so the replay meets the same
+        // buffer / extent state and the same request mix as the iteration
+        // (r02at: a replay through the probe buffer read ~5.5 GB/s where the
+        // iteration's reads into its per-checkpoint buffers got ~3 on the
+        // same virtio disk). Writes into the state / param files go to the
+        // probe file instead (the tier holds the initial states); every
+        // other request leaves no trace: reads return what the buffers
+        // already hold or what the iteration overwrites before use, and
+        // the activation / gradient extents are rewritten by the iteration
+        // before they are read. With warm_files two passes, the second one
+        // timed: the lane as every iteration after the first finds it.
+        constexpr std::uint64_t kReplay = 8ull << 30, kPerDir = 4ull << 30;
         double rd_b = 0, rd_s = 0, wr_b = 0, wr_s = 0;
-        std::uint64_t written = round_up(bytes);
         for (int pass = 0; pass < (opt_.warm_files ? 2 : 1); ++pass) {
             rd_b = rd_s = wr_b = wr_s = 0;
-            std::uint64_t wcur = round_up(bytes), rcur = 0, scur = 0;
+            std::uint64_t wcur = round_up(bytes);
             for (const Task& t : g_.tasks) {
-                if (t.resource != ResourceId::link_ssd || t.work <= 0.0) continue;
-                if (rd_b + wr_b >= double(kReplay)) break;
-                const std::uint64_t b = round_up(std::min<std::uint64_t>(static_cast<std::uint64_t>(t.work), bytes));
-                IoRequest op = w;
-                op.bytes = b;
-                op.write = t.dir == TransferDir::c2s;
-                if (op.write) {
-                    if (wcur + b > kReplay) wcur = 0;
+                FileOp fo;
+                if (!file_op(t, fo)) continue;
+                if (rd_b >= double(kPerDir) && wr_b >= double(kPerDir)) break;
+                if ((fo.write ? wr_b : rd_b) >= double(kPerDir)) continue;
+                IoRequest op{&io_, fo.file->stripe(), fo.buf, round_up(fo.bytes), fo.offset, fo.write, false,
+                             &io_error_, &io_error_text_, &io_mu_};
+                if (fo.write && (fo.file == f_states_.get() || fo.file == f_params_.get())) {
+                    if (wcur + op.bytes > kReplay) wcur = 0;
+                    op.file = probe_file.stripe();
                     op.offset = wcur;
-                    wcur += b;
-                    written = std::max(written, wcur);
-                } else if (f_states_ && tier_states_bytes_ >= b) {
-                    // reads come from the real states file (written at setup,
-                    // not since), like the iteration's own state reads, rather
-                    // than from probe data written a moment before
-                    if (scur + b > tier_states_bytes_) scur = 0;
-                    op.file = f_states_->stripe();
-                    op.offset = scur;
-                    scur += b;
-                } else {
-                    if (rcur + b > written) rcur = 0;
-                    op.offset = rcur;
-                    rcur += b;
+                    wcur += op.bytes;
                 }
                 const auto t0 = std::chrono::steady_clock::now();
                 run_io(&op);
-                const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-                (op.write ? wr_b : rd_b) += static_cast<double>(b);
+                const double sec =
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                (op.write ? wr_b : rd_b) += static_cast<double>(op.bytes);
                 (op.write ? wr_s : rd_s) += sec;
             }
         }
