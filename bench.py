@@ -90,7 +90,12 @@ def parse():
     ap.add_argument("--no-streamed", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streamed-chunks", type=int, default=6)
-    ap.add_argument("--streamed-pieces", type=int, default=16)  # r02ai: 0.891-0.894 vs 0.873 at 4
+    # r02ai: 16 pieces 0.891-0.894 vs 0.873 at 4; r02ay (interleaved): 32 pieces 3.569-3.571 G params/s
+    # vs 3.459-3.460 at 16 and 3.50-3.54 at 64
+    ap.add_argument("--streamed-pieces", type=int, default=32)
+    # streamed-shard phase: pieces of this many params (0: the streamed phase's piece size,
+    # one 65B chunk / --streamed-pieces), so both phases stream the same copy sizes
+    ap.add_argument("--shard-piece-params", type=int, default=0)
     ap.add_argument("--cpu-sample-chunks", type=int, default=4)  # = the reference arm's sample
     ap.add_argument("--no-swap-sweep", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1 / C4-block phase")
@@ -812,8 +817,8 @@ def streamed_shard_phase(torch, F, args, world, rank, local):
     (fy_shard_*, FY_TIER_HOST): GPT-3-175B-shaped blocks (1,811,939,328
     params) whose master/m/v live in each rank's NUMA-local pinned host
     memory (fy_host_alloc). Every block is sharded across the ranks; each
-    rank streams its slice through the library's chunk pipeline as 16 strided
-    pieces (12 B/param H2D, 12 B/param states + 2 B/param bf16 params D2H,
+    rank streams its slice through the library's chunk pipeline as strided
+    pieces of the streamed phase's size (12 B/param H2D, 12 B/param states + 2 B/param bf16 params D2H,
     grads in HBM) and the block's NCCL all-gather of the updated bf16 params
     runs on the shard's comm stream as soon as the block is updated,
     overlapping the next block's streaming. `args.shard_blocks` blocks per
@@ -824,8 +829,11 @@ def streamed_shard_phase(torch, F, args, world, rank, local):
     links = link_probe(torch, world, rank)
     dev = torch.device("cuda", local)
     sizes = [N4] * K
-    pieces = 16  # fill / drain = one piece each way: ~2% of the step at 16 pieces, ~10% at 4
+    # fill / drain = one piece each way: pieces of the streamed phase's size
+    # (r02ay: 25M params, 302 MB state copies) keep both to ~1% of the step
+    target = args.shard_piece_params or C3["chunk"] // args.streamed_pieces
     probe = F.optim.shard_range(N4, world, rank, 8)[1]
+    pieces = max(1, -(-probe // target))
     piece = max(8, (-(-probe // pieces) + 7) // 8 * 8)
     sh, gather, note = make_shard(torch, F, args, world, rank, local, sizes, "host", "nccl",
                                   slots=4, piece_elems=piece, params_to_host=True)
@@ -880,6 +888,7 @@ def streamed_shard_phase(torch, F, args, world, rank, local):
             "d2h_gbs_whole_job": d2h_total, "h2d_gbs_whole_job": h2d_total,
             "update_ms_per_step_rank0": upd_ms,
             "entry_point": "fy_shard_step (C ABI), FY_TIER_HOST",
+            "pieces_per_block_slice": pieces, "piece_params": piece,
             "gather": gather, "gather_note": note,
             "gather_bytes_per_rank_per_step": st["gather_bytes"],
             "links": links,
