@@ -166,6 +166,15 @@ def test_io_depth_option():
         assert st == 2 and "io_depth" in err
 
 
+def test_warm_files_option():
+    """warm_files (default true) is a bool exec option; a non-bool is a config error."""
+    for v in (True, False):
+        st, s, _, err = execute(C1, {"dry_run": True, "tier": "file", "warm_files": v})
+        assert st == 0, err
+    st, _, _, err = execute(C1, {"dry_run": True, "tier": "file", "warm_files": "yes"})
+    assert st == 2
+
+
 def _dry_trace(sc, opts):
     import json
     st, s, tr, err = execute(sc, {"dry_run": True, **opts}, want_trace=True)
