@@ -10,7 +10,7 @@
 // Build: g++ -O2 -std=c++20 -Ipaper_2403_06504_b200/csrc/core -I/usr/local/cuda/include \
 //        scripts/probes/file_rw_probe.cpp paper_2403_06504_b200/csrc/core/io_engine.cpp \
 //        -L/usr/local/cuda/lib64 -lcudart
-// argv[6] distinct (0/1), argv[7] pinned (0/1).
+// argv[6] distinct (0/1), argv[7] pinned (0/1), argv[8] link_load (0/1).
 #include "io_engine.hpp"
 
 #include <cuda_runtime.h>
@@ -19,6 +19,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -57,6 +58,10 @@ int main(int argc, char** argv) {
     // fy::host_alloc)
     const bool distinct = argc > 6 && std::atoi(argv[6]) != 0;
     const bool pinned = argc > 7 && std::atoi(argv[7]) != 0;
+    // link_load: a second thread keeps the GPU copy engines busy the whole
+    // time (1 = H2D + D2H 256 MiB copies from / to pinned host memory,
+    // back to back), as the executed iteration's copies are beside its file IO
+    const int link_load = argc > 8 ? std::atoi(argv[8]) : 0;
     const std::string path = dir + "/file_rw_probe.bin";
     int fd = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC | O_DIRECT, 0600);
     if (fd < 0) {
@@ -84,10 +89,39 @@ int main(int argc, char** argv) {
             q[i] = x;
         }
     }
+    std::atomic<bool> stop{false};
+    std::atomic<std::uint64_t> link_bytes{0};
+    std::thread loader;
+    if (link_load) {
+        loader = std::thread([&] {
+            const std::size_t lb = 256ull << 20;
+            void *hu = nullptr, *hd = nullptr, *du = nullptr, *dd = nullptr;
+            cudaHostAlloc(&hu, lb, cudaHostAllocDefault);
+            cudaHostAlloc(&hd, lb, cudaHostAllocDefault);
+            cudaMalloc(&du, lb);
+            cudaMalloc(&dd, lb);
+            cudaStream_t su, sd;
+            cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking);
+            cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
+            while (!stop.load()) {
+                cudaMemcpyAsync(du, hu, lb, cudaMemcpyHostToDevice, su);
+                cudaMemcpyAsync(hd, dd, lb, cudaMemcpyDeviceToHost, sd);
+                cudaStreamSynchronize(su);
+                cudaStreamSynchronize(sd);
+                link_bytes += 2 * lb;
+            }
+            cudaFree(du);
+            cudaFree(dd);
+            cudaFreeHost(hu);
+            cudaFreeHost(hd);
+        });
+        std::this_thread::sleep_for(std::chrono::milliseconds(200));
+    }
+    const double l0 = now();
     fy::IoEngine io(32, 4ull << 20);
     std::printf("{\"engine\": \"%s\", \"blocks\": %d, \"size\": %llu, \"random_data\": %d, \"distinct\": %d, "
-                "\"pinned\": %d}\n", io.engine(), blocks, static_cast<unsigned long long>(size), random_data ? 1 : 0,
-                distinct ? 1 : 0, pinned ? 1 : 0);
+                "\"pinned\": %d, \"link_load\": %d}\n", io.engine(), blocks, static_cast<unsigned long long>(size), random_data ? 1 : 0,
+                distinct ? 1 : 0, pinned ? 1 : 0, link_load);
     auto run = [&](const char* phase, bool write, bool reverse) {
         std::vector<double> t;
         for (int i = 0; i < blocks; ++i) {
@@ -113,6 +147,11 @@ int main(int argc, char** argv) {
     run("read_after_fsync_pause", false, true);
     run("read_again", false, true);
     run("read_forward_order", false, false);
+    if (link_load) {
+        stop = true;
+        loader.join();
+        std::printf("{\"link_load_gbs_both_ways\": %.2f}\n", link_bytes.load() / (now() - l0) / 1e9);
+    }
     ::close(fd);
     ::unlink(path.c_str());
     if (pinned) {
