@@ -205,6 +205,13 @@ struct MeasuredRates {
     // file tier: this graph's own file-lane operations replayed in task order
     double file_read_effective_bps = 0.0;
     double file_write_effective_bps = 0.0;
+    // ... and replayed again while both copy engines stream pinned host
+    // memory (GPU DMA contends with the file device for host memory)
+    double file_read_loaded_bps = 0.0;
+    double file_write_loaded_bps = 0.0;
+    // share of the file lane's planned busy time during which a link lane
+    // is busy (link_overlap on the planned trace)
+    double ssd_link_overlap = 0.0;
 };
 // Upper-bound rates (burst x 1.05): the issue order and the unchanged
 // roofline-lower-bound invariant on the real trace.

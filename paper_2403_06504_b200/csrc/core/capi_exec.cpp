@@ -206,6 +206,9 @@ json rates_json(const MeasuredRates& m) {
                 {"file_write_bps", m.file_write_bps},
                 {"file_read_effective_bps", m.file_read_effective_bps},
                 {"file_write_effective_bps", m.file_write_effective_bps},
+                {"file_read_loaded_bps", m.file_read_loaded_bps},
+                {"file_write_loaded_bps", m.file_write_loaded_bps},
+                {"ssd_link_overlap", m.ssd_link_overlap},
                 {"optimizer_params_per_s", m.optimizer_params_per_s},
                 {"compute_flops", m.compute_flops / m.compute_headroom},
                 {"compute_effective_flops", m.compute_effective_flops}};

@@ -313,10 +313,13 @@ HardwareConfig b200_hardware_effective(const HardwareConfig& planned_on, const M
     // (the binding one; the other lane then finishes early either way)
     hw.bw_gpu = r.c2g_bytes >= r.g2c_bytes ? up : down;
     if (r.c2g_bytes <= 0 && r.g2c_bytes <= 0) hw.bw_gpu = std::min(up, down);
+    // file lane: its requests replayed alone and under copy-engine load,
+    // blended the same way by the share of its planned busy time a link
+    // lane overlaps
     if (r.file_read_bps > 0)
-        hw.bw_s2c = r.file_read_effective_bps > 0 ? r.file_read_effective_bps : r.file_read_bps;
+        hw.bw_s2c = blend(r.file_read_effective_bps, r.file_read_loaded_bps, r.file_read_bps, r.ssd_link_overlap);
     if (r.file_write_bps > 0)
-        hw.bw_c2s = r.file_write_effective_bps > 0 ? r.file_write_effective_bps : r.file_write_bps;
+        hw.bw_c2s = blend(r.file_write_effective_bps, r.file_write_loaded_bps, r.file_write_bps, r.ssd_link_overlap);
     hw.cpu_opt_tput = r.optimizer_params_per_s;
     hw.gpu_tput = r.compute_effective_flops > 0 ? r.compute_effective_flops : r.compute_flops / r.compute_headroom;
     return hw;
@@ -355,10 +358,13 @@ namespace offsim {
 
 void link_overlap(const TaskGraph& graph, const SimTrace& trace, MeasuredRates& r) {
     // busy intervals per link lane (a lane is serial: its events do not overlap)
-    std::vector<std::pair<std::uint64_t, std::uint64_t>> up, down;
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> up, down, ssd, link;
     double ub = 0, db = 0;
     for (const TraceEvent& e : trace.events) {
         if (e.end_ns <= e.start_ns) continue;
+        if (e.resource == ResourceId::link_ssd) ssd.emplace_back(e.start_ns, e.end_ns);
+        if (e.resource == ResourceId::link_c2g || e.resource == ResourceId::link_g2c)
+            link.emplace_back(e.start_ns, e.end_ns);
         if (e.resource == ResourceId::link_c2g) {
             up.emplace_back(e.start_ns, e.end_ns);
             ub += graph.tasks[e.task_id].work;
@@ -385,6 +391,27 @@ void link_overlap(const TaskGraph& graph, const SimTrace& trace, MeasuredRates& 
     const double tu = total(up), td = total(down);
     r.c2g_overlap = tu > 0 ? both / tu : 0.0;
     r.g2c_overlap = td > 0 ? both / td : 0.0;
+    // file lane vs the union of the two link lanes (merged into disjoint
+    // intervals first: the link lanes overlap each other)
+    std::sort(ssd.begin(), ssd.end());
+    std::sort(link.begin(), link.end());
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> merged;
+    for (const auto& iv : link) {
+        if (!merged.empty() && iv.first <= merged.back().second)
+            merged.back().second = std::max(merged.back().second, iv.second);
+        else
+            merged.push_back(iv);
+    }
+    double ssd_both = 0;
+    for (std::size_t i = 0, j = 0; i < ssd.size() && j < merged.size();) {
+        const std::uint64_t lo = std::max(ssd[i].first, merged[j].first);
+        const std::uint64_t hi = std::min(ssd[i].second, merged[j].second);
+        if (hi > lo) ssd_both += static_cast<double>(hi - lo);
+        if (ssd[i].second < merged[j].second) ++i;
+        else ++j;
+    }
+    const double ts = total(ssd);
+    r.ssd_link_overlap = ts > 0 ? ssd_both / ts : 0.0;
     r.c2g_bytes = ub;
     r.g2c_bytes = db;
 }

@@ -32,6 +32,7 @@
 #include <atomic>
 #include <chrono>
 #include <set>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -916,15 +917,17 @@ MeasuredRates Engine::calibrate() {
         // before they are read. With warm_files two passes, the second one
         // timed: the lane as every iteration after the first finds it.
         constexpr std::uint64_t kReplay = 8ull << 30, kPerDir = 4ull << 30;
-        double rd_b = 0, rd_s = 0, wr_b = 0, wr_s = 0;
-        for (int pass = 0; pass < (opt_.warm_files ? 2 : 1); ++pass) {
-            rd_b = rd_s = wr_b = wr_s = 0;
+        struct Pass {
+            double rd_b = 0, rd_s = 0, wr_b = 0, wr_s = 0;
+        };
+        auto replay = [&]() {
+            Pass p;
             std::uint64_t wcur = round_up(bytes);
             for (const Task& t : g_.tasks) {
                 FileOp fo;
                 if (!file_op(t, fo)) continue;
-                if (rd_b >= double(kPerDir) && wr_b >= double(kPerDir)) break;
-                if ((fo.write ? wr_b : rd_b) >= double(kPerDir)) continue;
+                if (p.rd_b >= double(kPerDir) && p.wr_b >= double(kPerDir)) break;
+                if ((fo.write ? p.wr_b : p.rd_b) >= double(kPerDir)) continue;
                 IoRequest op{&io_, fo.file->stripe(), fo.buf, round_up(fo.bytes), fo.offset, fo.write, false,
                              &io_error_, &io_error_text_, &io_mu_};
                 if (fo.write && (fo.file == f_states_.get() || fo.file == f_params_.get())) {
@@ -937,12 +940,42 @@ MeasuredRates Engine::calibrate() {
                 run_io(&op);
                 const double sec =
                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-                (op.write ? wr_b : rd_b) += static_cast<double>(op.bytes);
-                (op.write ? wr_s : rd_s) += sec;
+                (op.write ? p.wr_b : p.rd_b) += static_cast<double>(op.bytes);
+                (op.write ? p.wr_s : p.rd_s) += sec;
             }
+            return p;
+        };
+        Pass alone;
+        for (int pass = 0; pass < (opt_.warm_files ? 2 : 1); ++pass) alone = replay();
+        if (alone.rd_s > 0) r.file_read_effective_bps = alone.rd_b / alone.rd_s;
+        if (alone.wr_s > 0) r.file_write_effective_bps = alone.wr_b / alone.wr_s;
+        // the same replay while both copy engines stream pinned host memory
+        // the whole time: GPU DMA into host memory slows the file lane (on
+        // the leases' virtio disk by ~22%, profiles/r02bc_file_rw_link_load.txt);
+        // tier_map blends the two by the share of the file lane's planned
+        // busy time a link lane overlaps (MeasuredRates::ssd_link_overlap)
+        bool has_link = false;
+        for (const Task& t : g_.tasks)
+            has_link |= t.work > 0.0 && (t.resource == ResourceId::link_c2g || t.resource == ResourceId::link_g2c);
+        const double t_alone = alone.rd_s + alone.wr_s;
+        if (has_link && t_alone > 0) {
+            constexpr std::uint64_t kCopy = 256ull << 20;
+            Pinned lh(kCopy), ld(kCopy);
+            Device du(kCopy), dd(kCopy);
+            const double rate = std::max(r.h2d_bps, r.d2h_bps) > 0 ? std::max(r.h2d_bps, r.d2h_bps) : 55e9;
+            const int copies = static_cast<int>(std::min(20000.0, std::ceil(1.5 * t_alone * rate / kCopy) + 2));
+            cudaStream_t su = lane_stream(ResourceId::link_c2g), sd = lane_stream(ResourceId::link_g2c);
+            for (int c = 0; c < copies; ++c) {
+                check_cuda(cudaMemcpyAsync(du.p, lh.p, kCopy, cudaMemcpyHostToDevice, su), "load H2D");
+                check_cuda(cudaMemcpyAsync(ld.p, dd.p, kCopy, cudaMemcpyDeviceToHost, sd), "load D2H");
+            }
+            std::this_thread::sleep_for(std::chrono::milliseconds(5));  // both engines running
+            const Pass loaded = replay();
+            check_cuda(cudaStreamSynchronize(su), "load H2D");
+            check_cuda(cudaStreamSynchronize(sd), "load D2H");
+            if (loaded.rd_s > 0) r.file_read_loaded_bps = loaded.rd_b / loaded.rd_s;
+            if (loaded.wr_s > 0) r.file_write_loaded_bps = loaded.wr_b / loaded.wr_s;
         }
-        if (rd_s > 0) r.file_read_effective_bps = rd_b / rd_s;
-        if (wr_s > 0) r.file_write_effective_bps = wr_b / wr_s;
         if (io_error_) throw InfeasibleError("file tier: " + io_error_text_);
     }
     r.compute_flops = opt_.compute_rate > 0 ? opt_.compute_rate : 0.0;

@@ -23,5 +23,8 @@ for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 5):
                           "ratio": ex / pr, "warmup_s": s.get("file_warmup_s"),
                           "read_eff_gbs": r["file_read_effective_bps"] / 1e9,
                           "write_eff_gbs": r["file_write_effective_bps"] / 1e9,
+                          "read_loaded_gbs": r.get("file_read_loaded_bps", 0) / 1e9,
+                          "write_loaded_gbs": r.get("file_write_loaded_bps", 0) / 1e9,
+                          "ssd_link_overlap": r.get("ssd_link_overlap"),
                           "legs": {k: round(v["gbs"], 2) for k, v in s["legs"].items() if "ssd" in k}}),
               flush=True)
