@@ -364,6 +364,7 @@ std::string dry_run_json(const Scenario& s, const ParsedOptions& po, ScheduleVar
                       {"analytic", analytic_json(mapped, hw, tr.makespan_s())},
                       {"link_overlap", json{{"c2g", overlap.c2g_overlap},
                                             {"g2c", overlap.g2c_overlap},
+                                            {"ssd_link", overlap.ssd_link_overlap},
                                             {"c2g_bytes", overlap.c2g_bytes},
                                             {"g2c_bytes", overlap.g2c_bytes}}},
                       {"invariants", checks},

@@ -175,6 +175,19 @@ def test_warm_files_option():
     assert st == 2
 
 
+def test_ssd_link_overlap_reported():
+    """The file lane's planned overlap with the link lanes (the weight of its
+    copy-engine-loaded replay): in [0, 1]; > 0 when states stream through
+    files and pinned memory at once; 0 on the host tier (no file lane)."""
+    st, s, _, err = execute(C1, {"dry_run": True, "tier": "file"})
+    assert st == 0, err
+    f = s["link_overlap"]["ssd_link"]
+    assert 0.0 < f <= 1.0, f
+    st, s, _, err = execute(C1, {"dry_run": True, "tier": "host"})
+    assert st == 0, err
+    assert s["link_overlap"]["ssd_link"] == 0.0
+
+
 def _dry_trace(sc, opts):
     import json
     st, s, tr, err = execute(sc, {"dry_run": True, **opts}, want_trace=True)
