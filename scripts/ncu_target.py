@@ -8,8 +8,14 @@ from pathlib import Path
 
 import torch
 
+# optional argv[1]: SM budget (fy_adamw_sm_budget CTAs) for the budgeted regime
+BUDGET = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2403_06504_b200 import optim as F  # noqa: E402
+from paper_2403_06504_b200._lib import LIB, check  # noqa: E402
+
+if BUDGET:
+    check(LIB.fy_adamw_sm_budget(BUDGET))
 
 N = 12 * 5120 * 5120
 dev = torch.device("cuda")
