@@ -21,7 +21,8 @@ ws = torch.zeros(F.workspace_floats(), device=dev)
 sq = torch.zeros(1, dtype=torch.float64, device=dev)
 hp = F.Hparams()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for budget in (32, 48, 64, 96, 128, 0):
+BUDGETS = [int(x) for x in sys.argv[2].split(',')] if len(sys.argv) > 2 else [32, 48, 64, 96, 128, 0]
+for budget in BUDGETS:
     check(LIB.fy_adamw_sm_budget(budget))
     best = 1e30
     for _ in range(3):
